@@ -1,0 +1,213 @@
+/*
+ * pfe_b200.h — C ABI of the B200-native piecewise-flat-embedding solver.
+ *
+ * Drop-in boundary for the reference's solver entry points in
+ * /root/reference/proj/core (namespace pfe).  Each function below names the
+ * reference interface it replaces.  Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary.
+ *
+ * Conventions
+ *   - Host matrices are column-major n x d (the reference's Eigen::MatrixXd,
+ *     solver.hpp:14).  Edge-indexed matrices (split_b, split_s) are |E| x d in
+ *     the caller's edge order (difference_matrix row order, graph.cpp:161-170).
+ *   - Status codes mirror the reference CLI's exception mapping
+ *     (proj/tools/main.cpp:431-446): 0 ok, 1 IoError, 2 NumericalError,
+ *     3 ConfigError; 4 = CUDA/driver failure.  pfe_last_error() returns the
+ *     message of the last failure on the calling thread.
+ *   - There is no CPU fallback: without a usable sm_100 device every entry
+ *     point that computes returns 3 with a message.
+ *   - A solver/state handle may be driven by one host thread at a time
+ *     (solver.hpp:51-83 is const and state is caller-owned).
+ */
+#ifndef PFE_B200_H
+#define PFE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFE_OK 0
+#define PFE_IO_ERROR 1
+#define PFE_NUMERICAL_ERROR 2
+#define PFE_CONFIG_ERROR 3
+#define PFE_CUDA_ERROR 4
+
+/* Preconditioner ids (pcg.hpp:13).  Ic0 runs the Jacobi path on the GPU and
+ * reports jacobi_fallback = 1, exactly as the reference does when its IC(0)
+ * factorization breaks down (pcg.cpp:22-28). */
+#define PFE_PRECOND_IC0 0
+#define PFE_PRECOND_JACOBI 1
+#define PFE_PRECOND_NONE 2
+
+/* Topology actually used by a solver (pfe_report.topology). */
+#define PFE_TOPO_CSR 0
+#define PFE_TOPO_GRID8 1  /* 3x3 neighbourhood stencil */
+#define PFE_TOPO_GRID24 2 /* 5x5 neighbourhood stencil */
+
+/* WeightedGraph (graph.hpp:15-28): undirected edges stored once with i < j,
+ * w finite; degree[] is used as given (solver.cpp:48-50) and must be > 0.
+ * Optional grid hint: when grid_h * grid_w == n and every edge is a forward
+ * stencil neighbour of radius grid_radius (1: 8-nbr, 2: 5x5) listed in
+ * lexicographic order, the solver uses the stencil kernels (no index
+ * arrays); otherwise it uses the general CSR kernels.  Results are identical
+ * either way. */
+typedef struct pfe_graph {
+  int32_t n;
+  int64_t m;
+  const int32_t* ei;
+  const int32_t* ej;
+  const double* w;
+  const double* degree;
+  int32_t grid_h;
+  int32_t grid_w;
+  int32_t grid_radius;
+} pfe_graph;
+
+/* PfeParams (solver.hpp:16-25) with PcgConfig (pcg.hpp:15-19) flattened.
+ * pfe_params_default() returns the reference defaults. */
+typedef struct pfe_params {
+  int32_t dim;
+  double lambda;
+  double r;
+  int32_t soc_max;
+  int32_t sb_max_stage1;
+  int32_t sb_max_stage2;
+  double conv_tol;
+  double pcg_rel_tol;
+  int32_t pcg_max_iter;
+  int32_t preconditioner;
+} pfe_params;
+
+/* Execution options (no reference counterpart). */
+typedef struct pfe_exec {
+  int32_t device;       /* CUDA ordinal */
+  int32_t use_graphs;   /* 1: capture the PCG loop as a CUDA graph with a
+                           device-side WHILE node (no host sync per PCG
+                           iteration); 0: host-driven loop */
+  int32_t warn;         /* 1: print the reference's non-converged-column
+                           warning to stderr (solver.cpp:87-92) */
+  int32_t profile;      /* 1: time every kernel launch with CUDA events */
+} pfe_exec;
+
+/* Run report (PcgReport aggregation, pcg.hpp:21-26). */
+typedef struct pfe_report {
+  int64_t inner_iterations;      /* split-Bregman iterations executed */
+  int64_t pcg_iterations;        /* sum over inner iterations of max-over-columns PCG iterations */
+  int64_t pcg_column_iterations; /* sum over inner iterations and columns */
+  int64_t nonconverged;          /* column solves that stopped unconverged (incl. failures) */
+  int64_t failed;                /* column solves that broke down (x kept at x0) */
+  int32_t jacobi_fallback;
+  int32_t topology;
+  int64_t n;
+  int64_t m;
+  int32_t d;
+  int32_t pad;
+  double setup_seconds;          /* host + device setup of pfe_solver_create */
+} pfe_report;
+
+/* Per-kernel-class timing when pfe_exec.profile = 1. */
+#define PFE_KERNEL_CLASSES 8
+/* 0 pcg_init, 1 pcg_spmv, 2 pcg_update, 3 pcg_finalize, 4 sb_pass,
+ * 5 rhs (quad / from state), 6 projection (tsqr + apply), 7 other */
+typedef struct pfe_kernel_times {
+  double ms[PFE_KERNEL_CLASSES];
+  int64_t launches[PFE_KERNEL_CLASSES];
+} pfe_kernel_times;
+
+typedef struct pfe_solver pfe_solver;
+typedef struct pfe_state pfe_state;
+
+/* IterateCallback (solver.hpp:36): Y (column-major host copy) after each
+ * inner iteration; forces the host-driven slow path. */
+typedef void (*pfe_iterate_fn)(int iteration, const double* y_colmajor, int32_t n, int32_t d, void* user);
+
+const char* pfe_last_error(void);
+pfe_params pfe_params_default(void);
+pfe_exec pfe_exec_default(void);
+int pfe_device_check(int32_t device); /* 0 if an sm_100-class device is usable */
+
+/* PfeSolver::PfeSolver (solver.hpp:53, solver.cpp:43-58): builds the
+ * operator A = (lambda/2) M^T M + (r/2) D, its Jacobi preconditioner and the
+ * graph topology on the device. */
+int pfe_solver_create(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, pfe_solver** out);
+void pfe_solver_destroy(pfe_solver* s);
+int pfe_solver_report(const pfe_solver* s, pfe_report* out);
+/* PCG log: per inner iteration x column iterations / status / final residual
+ * (status codes: 0 active, 1 converged, 2 zero rhs, 3 failed, 4 max_iter,
+ * 5 converged at x0).  Returns the number of logged inner iterations. */
+int64_t pfe_solver_pcg_log(const pfe_solver* s, int32_t* iters, int32_t* status, double* rel, int64_t cap);
+int pfe_solver_kernel_times(const pfe_solver* s, pfe_kernel_times* out, int reset);
+/* Device time (CUDA events on the solver's stream) of the last
+ * split_bregman / run_soc / two_stage call, in milliseconds. */
+double pfe_solver_last_ms(const pfe_solver* s);
+
+/* PfeSolver::make_state (solver.cpp:60-71): Y = y0, P = sqrt(D) y0, B = 0,
+ * split_b = split_s = 0.  y0 is host column-major n x dim. */
+int pfe_state_create(pfe_solver* s, const double* y0, pfe_state** out);
+/* Re-initialise an existing state from the y0 it was created with (device
+ * copy; no host transfer). */
+int pfe_state_reset(pfe_state* st);
+void pfe_state_destroy(pfe_state* st);
+
+/* SolverState fields (solver.hpp:28-34). */
+#define PFE_FIELD_Y 0
+#define PFE_FIELD_P 1
+#define PFE_FIELD_BREGMAN 2
+#define PFE_FIELD_SPLIT_B 3
+#define PFE_FIELD_SPLIT_S 4
+int pfe_state_get(pfe_state* st, int32_t field, double* out);
+int pfe_state_set(pfe_state* st, int32_t field, const double* in);
+
+/* PfeSolver::split_bregman (solver.cpp:73-108). */
+int pfe_split_bregman(pfe_solver* s, pfe_state* st, int32_t max_iter, pfe_iterate_fn cb, void* user);
+/* PfeSolver::run_soc (solver.cpp:110-126). */
+int pfe_run_soc(pfe_solver* s, pfe_state* st, int32_t soc_max, int32_t sb_max);
+/* PfeSolver::two_stage (solver.cpp:128-136) on a state fresh from make_state. */
+int pfe_two_stage(pfe_solver* s, pfe_state* st);
+/* objective(diff_matrix(), Y of the state) (solver.cpp:14-17). */
+int pfe_state_objective(pfe_solver* s, pfe_state* st, double* out);
+
+/* One-call drop-ins, host buffers in and out:
+ *   mode 0: soc(g, params, y0)            (solver.cpp:184-189)
+ *   mode 1: pfe_two_stage(g, params, y0)  (solver.cpp:191-193)          */
+int pfe_solve(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t mode, const double* y0,
+              double* y_out, pfe_report* rep);
+
+/* Standalone split_bregman(M, d_vec, P, B, params, y_init, max_iter, cb)
+ * (solver.cpp:138-182) with M = difference_matrix(g): fresh zero inner
+ * variables, operator built for this call. */
+int pfe_split_bregman_standalone(const pfe_graph* g, const double* p, const double* b, const pfe_params* prm,
+                                 int32_t d, const double* y_init, int32_t max_iter, const pfe_exec* x,
+                                 double* y_out, pfe_iterate_fn cb, void* user);
+
+/* PcgOperator(A, cfg).solve_multi(B, X0) (pcg.cpp:94-114) on a caller CSR
+ * matrix (row_ptr[n+1], col_idx, values; rows sorted, no duplicates as
+ * csr_from_triplets produces, sparse.hpp:17-25).  Per column: iterations,
+ * converged flag, final relative residual, jacobi_fallback. */
+int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, const double* values,
+                        int32_t d, const double* b, const double* x0, double rel_tol, int32_t max_iter,
+                        int32_t preconditioner, const pfe_exec* x, double* x_out, int32_t* iterations,
+                        int32_t* converged, double* residual, int32_t* jacobi_fallback);
+
+/* objective(M, Y) (solver.cpp:14-17) with M = difference_matrix(g). */
+int pfe_objective(const pfe_graph* g, int32_t d, const double* y, const pfe_exec* x, double* out);
+/* shrink(V, gamma) (solver.cpp:19-25), elementwise on count values. */
+int pfe_shrink(int64_t count, const double* v, double gamma, const pfe_exec* x, double* out);
+/* project_orthogonal(A) (solver.cpp:27-41): polar factor of n x d A. */
+int pfe_project_orthogonal(int32_t n, int32_t d, const double* a, const pfe_exec* x, double* p_out);
+
+/* Host-side boundary helpers (init.cpp:140-155, 172-181; cluster.cpp:54-124):
+ * seeded Y0 and the k-means "labels out" step, same RNG streams as the
+ * reference (std::mt19937_64 + libstdc++ distributions). */
+int pfe_d_orthonormalize(int32_t n, int32_t d, const double* a, const double* degree, double* out);
+int pfe_random_embedding(int32_t n, int32_t d, uint64_t seed, const double* degree, double* out);
+int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
+               int32_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PFE_B200_H */

@@ -1,0 +1,471 @@
+"""Python host mirror of the reference solver interface (namespace ``pfe`` in
+/root/reference/proj/core/include/pfe/*.hpp), backed by the sm_100a library.
+
+Same names, argument meaning and error behaviour as the reference:
+
+=====================================  ==========================================
+reference (C++)                        here
+=====================================  ==========================================
+``PfeParams`` (solver.hpp:16-25)        :class:`PfeParams`
+``PcgConfig`` / ``Preconditioner``      :class:`PcgConfig` / :class:`Preconditioner`
+``PcgReport`` (pcg.hpp:21-26)           :class:`PcgReport`
+``WeightedGraph`` (graph.hpp:15-28)     :class:`WeightedGraph`
+``SolverState`` (solver.hpp:28-34)      :class:`SolverState` (device resident)
+``PfeSolver`` (solver.hpp:51-83)        :class:`PfeSolver`
+``split_bregman`` free (solver.cpp:138) :func:`split_bregman`
+``soc`` / ``pfe_two_stage``             :func:`soc` / :func:`pfe_two_stage`
+``objective`` / ``shrink``              :func:`objective` / :func:`shrink`
+``project_orthogonal``                  :func:`project_orthogonal`
+``PcgOperator`` / ``pcg_solve_multi``   :class:`PcgOperator` / :func:`pcg_solve_multi`
+``random_embedding`` / ``d_orthonormalize`` (init.cpp:140-181)
+``kmeans`` (cluster.cpp:54-124)         :func:`kmeans` (labels out)
+``IoError`` / ``NumericalError`` / ``ConfigError`` (errors.hpp:9-24)
+=====================================  ==========================================
+
+Matrices are numpy ``(rows, d)`` float64 arrays; they are handed to the C ABI
+in column-major order (the reference's Eigen layout).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+
+
+class IoError(RuntimeError):
+    pass
+
+
+class NumericalError(RuntimeError):
+    pass
+
+
+class ConfigError(ValueError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_EXC = {N.PFE_IO_ERROR: IoError, N.PFE_NUMERICAL_ERROR: NumericalError, N.PFE_CONFIG_ERROR: ConfigError,
+        N.PFE_CUDA_ERROR: CudaError}
+
+
+def _check(rc: int) -> None:
+    if rc != N.PFE_OK:
+        msg = N.load().pfe_last_error().decode(errors="replace")
+        raise _EXC.get(rc, CudaError)(msg)
+
+
+class Preconditioner(enum.IntEnum):
+    Ic0 = 0
+    Jacobi = 1
+    NONE = 2
+
+
+@dataclass
+class PcgConfig:
+    rel_tol: float = 1e-6
+    max_iter: int = 1000
+    preconditioner: Preconditioner = Preconditioner.Ic0
+
+
+@dataclass
+class PcgReport:
+    iterations: int = 0
+    final_rel_residual: float = 0.0
+    converged: bool = False
+    jacobi_fallback: bool = False
+
+
+@dataclass
+class PfeParams:
+    dim: int = 5
+    lambda_: float = 100.0
+    r: float = 1.0
+    soc_max: int = 10
+    sb_max_stage1: int = 5
+    sb_max_stage2: int = 100
+    conv_tol: float = 1e-4
+    pcg: PcgConfig = field(default_factory=PcgConfig)
+
+    def to_c(self) -> N.pfe_params:
+        return N.pfe_params(int(self.dim), float(self.lambda_), float(self.r), int(self.soc_max),
+                            int(self.sb_max_stage1), int(self.sb_max_stage2), float(self.conv_tol),
+                            float(self.pcg.rel_tol), int(self.pcg.max_iter), int(self.pcg.preconditioner))
+
+
+@dataclass
+class WeightedGraph:
+    """Undirected graph, edges (i < j) in lexicographic order, degree used as given.
+
+    ``grid`` = (height, width, radius) marks a pixel grid whose edges are
+    stencil neighbours (radius 1: 8-neighbour, 2: 5x5); the solver then
+    uses the stencil kernels.  Results do not depend on the hint.
+    """
+    n: int
+    ei: np.ndarray
+    ej: np.ndarray
+    w: np.ndarray
+    degree: np.ndarray
+    sigma: float = 0.0
+    grid: Optional[Tuple[int, int, int]] = None
+
+    def __post_init__(self):
+        self.ei = np.ascontiguousarray(self.ei, dtype=np.int32)
+        self.ej = np.ascontiguousarray(self.ej, dtype=np.int32)
+        self.w = np.ascontiguousarray(self.w, dtype=np.float64)
+        self.degree = np.ascontiguousarray(self.degree, dtype=np.float64)
+
+    @property
+    def m(self) -> int:
+        return int(self.w.shape[0])
+
+    def edge_count(self) -> int:
+        return self.m
+
+    def to_c(self) -> N.pfe_graph:
+        h, w, r = self.grid if self.grid else (0, 0, 0)
+        return N.pfe_graph(int(self.n), int(self.m), N.iptr(self.ei), N.iptr(self.ej), N.dptr(self.w),
+                           N.dptr(self.degree), int(h), int(w), int(r))
+
+
+def degree_vector(ei, ej, w, n) -> np.ndarray:
+    """graph.cpp:15-22: weighted degree, accumulated in edge order."""
+    d = np.zeros(n)
+    for i, j, x in zip(np.asarray(ei), np.asarray(ej), np.asarray(w)):
+        d[i] += x
+        d[j] += x
+    return d
+
+
+def _exec(device=0, use_graphs=True, warn=True, profile=False) -> N.pfe_exec:
+    return N.pfe_exec(int(device), int(bool(use_graphs)), int(bool(warn)), int(bool(profile)))
+
+
+def _colmajor(a, rows=None, cols=None) -> np.ndarray:
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    if rows is not None and a.shape[0] != rows or cols is not None and a.shape[1] != cols:
+        raise ConfigError("PfeSolver: initial embedding has wrong shape")
+    return np.asfortranarray(a)
+
+
+def _from_colmajor(buf: np.ndarray, rows: int, cols: int) -> np.ndarray:
+    return np.array(buf.reshape(cols, rows).T, order="F")
+
+
+_FIELDS = {"y": 0, "p": 1, "bregman": 2, "split_b": 3, "split_s": 4}
+
+
+class SolverState:
+    """Device-resident SolverState; fields download on access, upload on assignment."""
+
+    def __init__(self, solver: "PfeSolver", handle: C.c_void_p):
+        self._solver = solver
+        self._h = handle
+
+    def _rows(self, name):
+        return self._solver.graph.m if name in ("split_b", "split_s") else self._solver.graph.n
+
+    def _get(self, name):
+        rows, d = self._rows(name), self._solver.params.dim
+        buf = np.empty(rows * d)
+        _check(N.load().pfe_state_get(self._h, _FIELDS[name], N.dptr(buf)))
+        return _from_colmajor(buf, rows, d)
+
+    def _set(self, name, value):
+        arr = _colmajor(value, self._rows(name), self._solver.params.dim)
+        _check(N.load().pfe_state_set(self._h, _FIELDS[name], N.dptr(arr)))
+
+    y = property(lambda s: s._get("y"), lambda s, v: s._set("y", v))
+    p = property(lambda s: s._get("p"), lambda s, v: s._set("p", v))
+    bregman = property(lambda s: s._get("bregman"), lambda s, v: s._set("bregman", v))
+    split_b = property(lambda s: s._get("split_b"), lambda s, v: s._set("split_b", v))
+    split_s = property(lambda s: s._get("split_s"), lambda s, v: s._set("split_s", v))
+
+    def reset(self) -> None:
+        """Back to make_state(y0) without a host transfer."""
+        _check(N.load().pfe_state_reset(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            N.load().pfe_state_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PfeSolver:
+    """PfeSolver (solver.hpp:51-83): operator, preconditioner and topology built once on the device."""
+
+    def __init__(self, graph: WeightedGraph, params: PfeParams, device: int = 0, use_graphs: bool = True,
+                 warn: bool = True, profile: bool = False):
+        lib = N.load()
+        self.graph = graph
+        self.params_ = params
+        self._g = graph.to_c()
+        self._p = params.to_c()
+        self._x = _exec(device, use_graphs, warn, profile)
+        h = C.c_void_p()
+        _check(lib.pfe_solver_create(C.byref(self._g), C.byref(self._p), C.byref(self._x), C.byref(h)))
+        self._h = h
+
+    @property
+    def params(self) -> PfeParams:
+        return self.params_
+
+    def diff_matrix(self) -> WeightedGraph:
+        return self.graph
+
+    def make_state(self, y0) -> SolverState:
+        arr = _colmajor(y0, self.graph.n, self.params.dim)
+        h = C.c_void_p()
+        _check(N.load().pfe_state_create(self._h, N.dptr(arr), C.byref(h)))
+        return SolverState(self, h)
+
+    def split_bregman(self, state: SolverState, max_iter: int,
+                      on_iterate: Optional[Callable[[int, np.ndarray], None]] = None) -> None:
+        cb = N.ITERATE_FN()
+        keep = None
+        if on_iterate is not None:
+            def _tramp(it, yp, n, d, _user):
+                y = np.ctypeslib.as_array(yp, shape=(n * d,)).copy()
+                on_iterate(int(it), _from_colmajor(y, n, d))
+            keep = N.ITERATE_FN(_tramp)
+            cb = keep
+        _check(N.load().pfe_split_bregman(self._h, state._h, int(max_iter), cb, None))
+        del keep
+
+    def run_soc(self, state: SolverState, soc_max: int, sb_max: int) -> None:
+        _check(N.load().pfe_run_soc(self._h, state._h, int(soc_max), int(sb_max)))
+
+    def two_stage(self, y0) -> SolverState:
+        st = self.make_state(y0)
+        _check(N.load().pfe_two_stage(self._h, st._h))
+        return st
+
+    def objective(self, state: SolverState) -> float:
+        out = C.c_double()
+        _check(N.load().pfe_state_objective(self._h, state._h, C.byref(out)))
+        return out.value
+
+    def report(self) -> dict:
+        r = N.pfe_report()
+        _check(N.load().pfe_solver_report(self._h, C.byref(r)))
+        return {k: getattr(r, k) for k, _ in N.pfe_report._fields_ if k != "pad"}
+
+    def pcg_log(self):
+        d = self.params.dim
+        cap = 1 << 20
+        n = self.report()["inner_iterations"]
+        cap = max(1, n)
+        it = np.zeros(cap * d, np.int32)
+        st = np.zeros(cap * d, np.int32)
+        rel = np.zeros(cap * d)
+        cnt = N.load().pfe_solver_pcg_log(self._h, N.iptr(it), N.iptr(st), N.dptr(rel), cap)
+        if cnt < 0:
+            _check(int(-cnt))
+        return it[:cnt * d].reshape(cnt, d), st[:cnt * d].reshape(cnt, d), rel[:cnt * d].reshape(cnt, d)
+
+    def last_ms(self) -> float:
+        """Device time (CUDA events on the solver stream) of the last solver call."""
+        return float(N.load().pfe_solver_last_ms(self._h))
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        t = N.pfe_kernel_times()
+        _check(N.load().pfe_solver_kernel_times(self._h, C.byref(t), int(reset)))
+        return {name: (t.ms[i], int(t.launches[i])) for i, name in enumerate(N.KERNEL_CLASSES)}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.load().pfe_solver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _solve(mode: int, g: WeightedGraph, params: PfeParams, y0, device=0, use_graphs=True):
+    y0c = _colmajor(y0, g.n, params.dim)
+    out = np.empty(g.n * params.dim)
+    gc, pc, xc = g.to_c(), params.to_c(), _exec(device, use_graphs)
+    rep = N.pfe_report()
+    _check(N.load().pfe_solve(C.byref(gc), C.byref(pc), C.byref(xc), mode, N.dptr(y0c), N.dptr(out),
+                              C.byref(rep)))
+    return _from_colmajor(out, g.n, params.dim)
+
+
+def soc(g: WeightedGraph, params: PfeParams, y0, **kw) -> np.ndarray:
+    """soc(g, params, y0) (solver.cpp:184-189)."""
+    return _solve(0, g, params, y0, **kw)
+
+
+def pfe_two_stage(g: WeightedGraph, params: PfeParams, y0, **kw) -> np.ndarray:
+    """pfe_two_stage(g, params, y0) (solver.cpp:191-193)."""
+    return _solve(1, g, params, y0, **kw)
+
+
+def split_bregman(g: WeightedGraph, d_vec, p, b, params: PfeParams, y_init, max_iter: int,
+                  on_iterate: Optional[Callable[[int, np.ndarray], None]] = None, device: int = 0) -> np.ndarray:
+    """Standalone split_bregman with M = difference_matrix(g) (solver.cpp:138-182)."""
+    y_init = np.asarray(y_init, dtype=np.float64)
+    if y_init.ndim == 1:
+        y_init = y_init.reshape(-1, 1)
+    n, d = y_init.shape
+    gg = WeightedGraph(g.n, g.ei, g.ej, g.w, np.asarray(d_vec, dtype=np.float64), grid=g.grid)
+    gc = gg.to_c()
+    pc = params.to_c()
+    xc = _exec(device, True, False)
+    pa, ba, ya = _colmajor(p, n, d), _colmajor(b, n, d), _colmajor(y_init, n, d)
+    out = np.empty(n * d)
+    cb = N.ITERATE_FN()
+    keep = None
+    if on_iterate is not None:
+        def _tramp(it, yp, nn, dd, _user):
+            on_iterate(int(it), _from_colmajor(np.ctypeslib.as_array(yp, shape=(nn * dd,)).copy(), nn, dd))
+        keep = N.ITERATE_FN(_tramp)
+        cb = keep
+    _check(N.load().pfe_split_bregman_standalone(C.byref(gc), N.dptr(pa), N.dptr(ba), C.byref(pc), d, N.dptr(ya),
+                                                 int(max_iter), C.byref(xc), N.dptr(out), cb, None))
+    del keep
+    return _from_colmajor(out, n, d)
+
+
+def objective(g: WeightedGraph, y, device: int = 0) -> float:
+    """objective(difference_matrix(g), Y) = sum_edges w |y_i - y_j|_1 (solver.cpp:14-17)."""
+    y = np.asarray(y, dtype=np.float64)
+    if y.ndim == 1:
+        y = y.reshape(-1, 1)
+    if y.shape[0] != g.n:
+        raise ConfigError("objective: dimension mismatch")
+    gc, xc = g.to_c(), _exec(device)
+    ya = _colmajor(y)
+    out = C.c_double()
+    _check(N.load().pfe_objective(C.byref(gc), y.shape[1], N.dptr(ya), C.byref(xc), C.byref(out)))
+    return out.value
+
+
+def shrink(v, gamma: float, device: int = 0) -> np.ndarray:
+    """shrink(V, gamma) = sign(v) max(|v| - gamma, 0) elementwise (solver.cpp:19-25)."""
+    v = np.asarray(v, dtype=np.float64)
+    flat = np.ascontiguousarray(v).reshape(-1)
+    out = np.empty_like(flat)
+    xc = _exec(device)
+    _check(N.load().pfe_shrink(flat.size, N.dptr(flat), float(gamma), C.byref(xc), N.dptr(out)))
+    return out.reshape(v.shape)
+
+
+def project_orthogonal(a, device: int = 0) -> np.ndarray:
+    """Frobenius-nearest matrix with orthonormal columns (solver.cpp:27-41)."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    n, d = a.shape
+    if n < d:
+        raise ConfigError("project_orthogonal: need rows >= cols")
+    ac = _colmajor(a)
+    out = np.empty(n * d)
+    xc = _exec(device)
+    _check(N.load().pfe_project_orthogonal(n, d, N.dptr(ac), C.byref(xc), N.dptr(out)))
+    return _from_colmajor(out, n, d)
+
+
+class PcgOperator:
+    """PcgOperator(A, cfg) (pcg.hpp:31-54) over a CSR matrix (row_ptr, col_idx, values)."""
+
+    def __init__(self, a, cfg: PcgConfig, device: int = 0):
+        row_ptr, col_idx, values = a
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        self.col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        self.n = self.row_ptr.size - 1
+        if cfg.rel_tol <= 0.0:
+            raise ConfigError("PcgOperator: rel_tol must be > 0")
+        if cfg.max_iter < 1:
+            raise ConfigError("PcgOperator: max_iter must be >= 1")
+        self.cfg = cfg
+        self.device = device
+
+    def solve_multi(self, b, x0) -> Tuple[np.ndarray, List[PcgReport]]:
+        b = np.asarray(b, dtype=np.float64)
+        x0 = np.asarray(x0, dtype=np.float64)
+        if b.ndim == 1:
+            b = b.reshape(-1, 1)
+        if x0.ndim == 1:
+            x0 = x0.reshape(-1, 1)
+        if b.shape[0] != self.n or x0.shape[0] != self.n or b.shape[1] != x0.shape[1]:
+            raise ConfigError("pcg_solve_multi: dimension mismatch")
+        d = b.shape[1]
+        bc, xc0 = _colmajor(b), _colmajor(x0)
+        out = np.empty(self.n * d)
+        its = np.zeros(d, np.int32)
+        conv = np.zeros(d, np.int32)
+        res = np.zeros(d)
+        fb = np.zeros(d, np.int32)
+        xc = _exec(self.device, True, False)
+        _check(N.load().pfe_pcg_solve_multi(self.n, N.iptr(self.row_ptr), N.iptr(self.col_idx), N.dptr(self.values),
+                                            d, N.dptr(bc), N.dptr(xc0), float(self.cfg.rel_tol),
+                                            int(self.cfg.max_iter), int(self.cfg.preconditioner), C.byref(xc),
+                                            N.dptr(out), N.iptr(its), N.iptr(conv), N.dptr(res), N.iptr(fb)))
+        reps = [PcgReport(int(its[j]), float(res[j]), bool(conv[j]), bool(fb[j])) for j in range(d)]
+        return _from_colmajor(out, self.n, d), reps
+
+    def solve(self, b, x0) -> Tuple[np.ndarray, PcgReport]:
+        x, reps = self.solve_multi(np.asarray(b).reshape(-1, 1), np.asarray(x0).reshape(-1, 1))
+        return x[:, 0], reps[0]
+
+
+def pcg_solve_multi(a, b, x0, cfg: PcgConfig, device: int = 0):
+    """pcg_solve_multi (pcg.cpp:122-127)."""
+    return PcgOperator(a, cfg, device).solve_multi(b, x0)
+
+
+def pcg_solve(a, b, x0, cfg: PcgConfig, device: int = 0):
+    """pcg_solve (pcg.cpp:116-120)."""
+    return PcgOperator(a, cfg, device).solve(b, x0)
+
+
+def random_embedding(n: int, d: int, seed: int, degree) -> np.ndarray:
+    """random_embedding (init.cpp:172-181): mt19937_64 + libstdc++ normal, D-orthonormalized."""
+    deg = np.ascontiguousarray(degree, dtype=np.float64)
+    out = np.empty(n * d)
+    _check(N.load().pfe_random_embedding(int(n), int(d), int(seed) & ((1 << 64) - 1), N.dptr(deg), N.dptr(out)))
+    return _from_colmajor(out, n, d)
+
+
+def d_orthonormalize(a, degree) -> np.ndarray:
+    """d_orthonormalize (init.cpp:140-155)."""
+    a = np.asarray(a, dtype=np.float64)
+    n, d = a.shape
+    deg = np.ascontiguousarray(degree, dtype=np.float64)
+    ac = _colmajor(a)
+    out = np.empty(n * d)
+    _check(N.load().pfe_d_orthonormalize(n, d, N.dptr(ac), N.dptr(deg), N.dptr(out)))
+    return _from_colmajor(out, n, d)
+
+
+def kmeans(points, k: int, seed: int, max_iter: int = 100) -> np.ndarray:
+    """kmeans (cluster.cpp:54-124): k-means++ seeding + Lloyd; returns labels."""
+    pts = np.asarray(points, dtype=np.float64)
+    if pts.ndim == 1:
+        pts = pts.reshape(-1, 1)
+    n, d = pts.shape
+    pc = _colmajor(pts)
+    lab = np.zeros(n, np.int32)
+    _check(N.load().pfe_kmeans(n, d, N.dptr(pc), int(k), int(seed), int(max_iter), N.iptr(lab)))
+    return lab

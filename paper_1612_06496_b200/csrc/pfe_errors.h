@@ -1,0 +1,20 @@
+// Error type carried from the implementation to the C ABI status codes
+// (errors.hpp:9-24 -> proj/tools/main.cpp:431-446 numbering).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace pfe_host {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void random_embedding(int n, int d, uint64_t seed, const double* deg, double* out);
+void d_orthonormalize(int n, int d, const double* a, const double* deg, double* out);
+void kmeans(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
+
+}  // namespace pfe_host

@@ -1,0 +1,463 @@
+// Hot-path kernels of the PFE nested Bregman loop (templates; instantiated per
+// topology and embedding dimension in pfe_kernels_*.cu).
+//
+//   k_pcg_init    r = b - A x0, p = D^-1 r, ||b||^2, r.r, r.z      (pcg.cpp:49-66)
+//   k_pcg_spmv    p = D^-1 r + beta p (fused), q = A p, p.q, alpha (pcg.cpp:68-72, 86-88)
+//   k_pcg_update  x += alpha p, r -= alpha q, r.r, r.D^-1 r, beta  (pcg.cpp:73-85)
+//   k_pcg_finalize  per-column result selection + PCG log          (pcg.cpp:50-53, 56-62, 101-112)
+//   k_sb_pass     M Y, shrink, Bregman b update, next rhs           (solver.cpp:83-84, 96-98)
+//   k_rhs_quad / k_rhs_from_state                                   (solver.cpp:79-84)
+//   k_objective   sum |M Y|                                         (solver.cpp:14-17)
+// All d columns are iterated together; each column keeps its own alpha,
+// beta, residual and stopping state exactly as solve_multi runs them one by
+// one (pcg.cpp:94-114).  Kernels read the PCG iteration index from the
+// device control block, so the same launch sequence works inside a CUDA
+// graph whose PCG loop is a conditional WHILE node.
+#pragma once
+
+#include "pfe_device.cuh"
+
+namespace pfe_dev {
+
+struct PcgArgs {
+  const double* x0;    // Y (warm start), row-major [n][D]
+  double* x;           // Y2: solve result buffer
+  const double* rhs;   // right-hand side (may alias r)
+  double* r;
+  double* pbuf[2];     // ping-pong search directions
+  double* q;
+  Ctl* ctl;
+  double* partials;
+  double tol;
+  int max_iter;
+  cudaGraphConditionalHandle cond;  // loop handle when running inside a graph
+  int use_cond;
+};
+
+// ---------------------------------------------------------------- PCG init --
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  double acc[3][V] = {};
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    double ax[V] = {};
+    topo.visitA(v, [&](int u, double av) {
+      const Row<V> xu = ldg_row<V>(a.x0 + static_cast<long>(u) * D + c0);
+#pragma unroll
+      for (int k = 0; k < V; ++k) ax[k] += av * xu.a[k];
+    });
+    const Row<V> b = ld_row<V>(a.rhs + static_cast<long>(v) * D + c0);
+    const double id = topo.inv_diag(v);
+    Row<V> r, z;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      r.a[k] = b.a[k] - ax[k];
+      z.a[k] = id * r.a[k];
+      acc[0][k] += b.a[k] * b.a[k];
+      acc[1][k] += r.a[k] * r.a[k];
+      acc[2][k] += r.a[k] * z.a[k];
+    }
+    st_row<V>(a.r + static_cast<long>(v) * D + c0, r);
+    st_row<V>(a.pbuf[0] + static_cast<long>(v) * D + c0, z);
+  }
+  block_reduce_store<3, D, V>(acc, a.partials);
+  __shared__ double tot[3][D];
+  if (!grid_reduce_last<3, D>(a.partials, a.ctl, tot)) return;
+  if (threadIdx.x == 0) {
+    Ctl* c = a.ctl;
+    int any = 0, fix = 0;
+    for (int j = 0; j < D; ++j) {
+      PcgCol& col = c->col[j];
+      col.bnorm = sqrt(tot[0][j]);
+      col.iters = 0;
+      col.alpha = col.beta = col.pq = 0.0;
+      if (col.bnorm == 0.0) {
+        col.status = kZeroRhs;
+        col.rel = 0.0;
+      } else {
+        col.rel = sqrt(tot[1][j]) / col.bnorm;
+        if (col.rel <= a.tol) {
+          col.status = kConvInit;
+        } else {
+          col.status = kActive;
+          col.rz = tot[2][j];
+        }
+      }
+      any |= (col.status == kActive);
+      fix |= (col.status != kActive);
+    }
+    c->iter = 0;
+    c->any_active = any;
+    c->need_fix = fix;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
+  }
+}
+
+// ------------------------------------------------------- PCG SpMV (+ p update)
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  const Ctl* c = a.ctl;
+  if (!c->any_active) return;
+  const int it = c->iter + 1;
+  const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
+  double beta[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) beta[k] = (c->col[gfirst + k].status == kActive) ? c->col[gfirst + k].beta : 0.0;
+  double* pnew = (it & 1) ? a.pbuf[0] : a.pbuf[1];
+  const double* pold = (it & 1) ? a.pbuf[1] : a.pbuf[0];
+  double acc[1][V] = {};
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    double q[V] = {};
+    Row<V> pv;
+    if (it == 1) {
+      pv = ldg_row<V>(pnew + static_cast<long>(v) * D + c0);
+      topo.visitA(v, [&](int u, double av) {
+        const Row<V> pu = ldg_row<V>(pnew + static_cast<long>(u) * D + c0);
+#pragma unroll
+        for (int k = 0; k < V; ++k) q[k] += av * pu.a[k];
+      });
+    } else {
+      // p_u = z_u + beta p_u with z_u = D^-1_u r_u, recomputed identically
+      // for every row that reads vertex u (pcg.cpp:86-88).
+      auto pdir = [&](int u) {
+        const Row<V> ru = ldg_row<V>(a.r + static_cast<long>(u) * D + c0);
+        const Row<V> po = ldg_row<V>(pold + static_cast<long>(u) * D + c0);
+        const double id = topo.inv_diag(u);
+        Row<V> pu;
+#pragma unroll
+        for (int k = 0; k < V; ++k) pu.a[k] = id * ru.a[k] + beta[k] * po.a[k];
+        return pu;
+      };
+      pv = pdir(v);
+      topo.visitA(v, [&](int u, double av) {
+        const Row<V> pu = pdir(u);
+#pragma unroll
+        for (int k = 0; k < V; ++k) q[k] += av * pu.a[k];
+      });
+      st_row<V>(pnew + static_cast<long>(v) * D + c0, pv);
+    }
+    Row<V> qv;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      qv.a[k] = q[k];
+      acc[0][k] += pv.a[k] * q[k];
+    }
+    st_row<V>(a.q + static_cast<long>(v) * D + c0, qv);
+  }
+  block_reduce_store<1, D, V>(acc, a.partials);
+  __shared__ double tot[1][D];
+  if (!grid_reduce_last<1, D>(a.partials, a.ctl, tot)) return;
+  if (threadIdx.x == 0) {
+    Ctl* cw = a.ctl;
+    for (int j = 0; j < D; ++j) {
+      PcgCol& col = cw->col[j];
+      if (col.status != kActive) continue;
+      const double pq = tot[0][j];
+      col.pq = pq;
+      if (!(pq > 0.0) || !isfinite(pq)) {  // pcg.cpp:71-72
+        col.status = kFailed;
+        col.iters = 0;
+        col.rel = __longlong_as_double(0x7ff0000000000000ll);
+        cw->need_fix = 1;
+      } else {
+        col.alpha = col.rz / pq;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- PCG update -----
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  const Ctl* c = a.ctl;
+  if (!c->any_active) return;
+  const int it = c->iter + 1;
+  const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
+  double alpha[V];
+  bool act[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    act[k] = c->col[gfirst + k].status == kActive;
+    alpha[k] = act[k] ? c->col[gfirst + k].alpha : 0.0;
+  }
+  const double* xsrc = (it == 1) ? a.x0 : a.x;
+  const double* pin = (it & 1) ? a.pbuf[0] : a.pbuf[1];
+  double acc[3][V] = {};
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    const long o = static_cast<long>(v) * D + c0;
+    Row<V> x = ld_row<V>(xsrc + o);
+    Row<V> r = ld_row<V>(a.r + o);
+    const Row<V> p = ldg_row<V>(pin + o);
+    const Row<V> q = ldg_row<V>(a.q + o);
+    const double id = topo.inv_diag(v);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      if (act[k]) {
+        x.a[k] = x.a[k] + alpha[k] * p.a[k];
+        r.a[k] = r.a[k] - alpha[k] * q.a[k];
+        if (!isfinite(x.a[k])) acc[2][k] += 1.0;
+      }
+      const double z = id * r.a[k];
+      acc[0][k] += r.a[k] * r.a[k];
+      acc[1][k] += r.a[k] * z;
+    }
+    st_row<V>(a.x + o, x);
+    st_row<V>(a.r + o, r);
+  }
+  block_reduce_store<3, D, V>(acc, a.partials);
+  __shared__ double tot[3][D];
+  if (!grid_reduce_last<3, D>(a.partials, a.ctl, tot)) return;
+  if (threadIdx.x == 0) {
+    Ctl* cw = a.ctl;
+    int any = 0;
+    for (int j = 0; j < D; ++j) {
+      PcgCol& col = cw->col[j];
+      if (col.status != kActive) continue;
+      if (tot[2][j] > 0.0) {  // pcg.cpp:75
+        col.status = kFailed;
+        col.iters = 0;
+        col.rel = __longlong_as_double(0x7ff0000000000000ll);
+        cw->need_fix = 1;
+        continue;
+      }
+      col.rel = sqrt(tot[0][j]) / col.bnorm;
+      col.iters = it;
+      if (col.rel <= a.tol) {
+        col.status = kConverged;
+      } else if (it >= a.max_iter) {
+        col.status = kMaxIter;
+      } else {
+        col.beta = tot[1][j] / col.rz;
+        col.rz = tot[1][j];
+        any = 1;
+      }
+    }
+    cw->iter = it;
+    cw->any_active = any;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
+  }
+}
+
+// --------------------------------------------------------- PCG finalize -----
+// Columns that never iterated (zero rhs / converged at x0) or that broke down
+// take their value from x0 / zero; every other column is already in x.  Also
+// appends the per-column report of this solve to the PCG log.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_pcg_finalize(int n, const double* __restrict__ x0, double* x, Ctl* ctl) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int idx = ctl->inner_count;
+    if (idx < ctl->log_cap) {
+      for (int j = 0; j < D; ++j) {
+        ctl->log_iters[static_cast<long>(idx) * D + j] = ctl->col[j].iters;
+        ctl->log_status[static_cast<long>(idx) * D + j] = ctl->col[j].status;
+        ctl->log_rel[static_cast<long>(idx) * D + j] = ctl->col[j].rel;
+      }
+    }
+  }
+  if (!ctl->need_fix) return;
+  const bool never_iterated = ctl->iter == 0;
+  int mode[D];  // 0 keep, 1 from x0, 2 zero
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const int st = ctl->col[j].status;
+    mode[j] = st == kZeroRhs ? 2 : ((st == kConvInit || st == kFailed || never_iterated) ? 1 : 0);
+  }
+  const long total = static_cast<long>(n) * D;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int j = static_cast<int>(e % D);
+    if (mode[j] == 1) x[e] = x0[e];
+    else if (mode[j] == 2) x[e] = 0.0;
+  }
+}
+
+// Bumps the inner-iteration counter (separate tiny launch so that every
+// block of k_pcg_finalize has read the control block before it changes).
+static __global__ void k_inner_done(Ctl* ctl) {
+  if (threadIdx.x == 0) ctl->inner_count += 1;
+}
+
+// ----------------------------------------------------- split-Bregman pass ---
+struct SbArgs {
+  const double* y;      // new Y
+  const double* b_old;  // null => zero
+  double* b_new;
+  double* s_out;        // null => do not materialize split_s
+  const double* rq;     // rhs_quad
+  double* rhs;          // null => do not produce the next rhs
+  double hl;            // lambda / 2
+  double gamma;         // 1 / lambda
+  Ctl* ctl;
+};
+
+// Per vertex v and column group: for every incident edge e (ascending edge
+// index): my_e = w y_i + (-w) y_j (spmm_dense over M, sparse.cpp:77-83),
+// s_e = shrink(my_e + b_e) (solver.cpp:97), b_e' = b_e + (my_e - s_e)
+// (solver.cpp:98); the owner (v == i) stores b_e' (and s_e).  The next
+// right-hand side (solver.cpp:83-84) is accumulated from the same edge values:
+// rhs_v = hl * sum_e M_ev (s_e - b_e') + rq_v.
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_sb_pass(Topo topo, SbArgs a) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  int bad = 0;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    const Row<V> yv = ldg_row<V>(a.y + static_cast<long>(v) * D + c0);
+#pragma unroll
+    for (int k = 0; k < V; ++k) bad |= !isfinite(yv.a[k]);
+    double acc[V] = {};
+    topo.visitE(v, [&](int u, double w, long slot, bool fwd) {
+      const Row<V> yu = ldg_row<V>(a.y + static_cast<long>(u) * D + c0);
+      Row<V> bo;
+      if (a.b_old) {
+        bo = ldg_row<V>(a.b_old + slot * D + c0);
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; ++k) bo.a[k] = 0.0;
+      }
+      Row<V> bn, sv;
+      const double nw = -w;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const double yi = fwd ? yv.a[k] : yu.a[k];
+        const double yj = fwd ? yu.a[k] : yv.a[k];
+        const double t1 = w * yi;
+        const double my = t1 + nw * yj;
+        const double s = shrink1(my + bo.a[k], a.gamma);
+        bn.a[k] = bo.a[k] + (my - s);
+        sv.a[k] = s;
+        acc[k] += (fwd ? w : nw) * (s - bn.a[k]);
+      }
+      if (fwd) {
+        st_row<V>(a.b_new + slot * D + c0, bn);
+        if (a.s_out) st_row<V>(a.s_out + slot * D + c0, sv);
+      }
+    });
+    if (a.rhs) {
+      const Row<V> rq = ldg_row<V>(a.rq + static_cast<long>(v) * D + c0);
+      Row<V> out;
+#pragma unroll
+      for (int k = 0; k < V; ++k) out.a[k] = a.hl * acc[k] + rq.a[k];
+      st_row<V>(a.rhs + static_cast<long>(v) * D + c0, out);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.ctl->nonfinite_y, 1);
+}
+
+// rhs_v = hl * sum_e M_ev (s_e - b_e) + rq_v for a caller-supplied inner
+// state (first iteration of split_bregman when b, s are not known zero).
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_rhs_from_state(Topo topo, const double* __restrict__ s,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ rq, double* rhs, double hl) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    double acc[V] = {};
+    topo.visitE(v, [&](int, double w, long slot, bool fwd) {
+      const Row<V> sv = ldg_row<V>(s + slot * D + c0);
+      const Row<V> bv = ldg_row<V>(b + slot * D + c0);
+      const double coef = fwd ? w : -w;
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] += coef * (sv.a[k] - bv.a[k]);
+    });
+    const Row<V> q = ldg_row<V>(rq + static_cast<long>(v) * D + c0);
+    Row<V> out;
+#pragma unroll
+    for (int k = 0; k < V; ++k) out.a[k] = hl * acc[k] + q.a[k];
+    st_row<V>(rhs + static_cast<long>(v) * D + c0, out);
+  }
+}
+
+// rq = (r/2) * (sqrt(deg) * (P - B))   (solver.cpp:79-80)
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_rhs_quad(int n, const double* __restrict__ sqd, const double* __restrict__ p,
+                                                    const double* __restrict__ breg, double* rq, double hr) {
+  const long total = static_cast<long>(n) * D;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / D);
+    rq[e] = hr * (__ldg(sqd + v) * (__ldg(p + e) - __ldg(breg + e)));
+  }
+}
+
+// objective = sum over edges and columns of |w y_i + (-w) y_j| (solver.cpp:14-17).
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_objective(Topo topo, const double* __restrict__ y, double* partials,
+                                                     Ctl* ctl) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  double acc[1][V] = {};
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    const Row<V> yv = ldg_row<V>(y + static_cast<long>(v) * D + c0);
+    topo.visitE(v, [&](int u, double w, long, bool fwd) {
+      if (!fwd) return;
+      const Row<V> yu = ldg_row<V>(y + static_cast<long>(u) * D + c0);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[0][k] += fabs(w * yv.a[k] + (-w) * yu.a[k]);
+    });
+  }
+  block_reduce_store<1, D, V>(acc, partials);
+  __shared__ double tot[1][D];
+  if (!grid_reduce_last<1, D>(partials, ctl, tot)) return;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int j = 0; j < D; ++j) s += tot[0][j];
+    ctl->scalar[0] = s;
+  }
+}
+
+// ||Y_new - Y_old||^2 and ||Y_old||^2 for the relative-change test
+// (solver.cpp:102-106, 120-124).
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_diff_norms(int n, const double* __restrict__ ynew,
+                                                      const double* __restrict__ yold, double* partials, Ctl* ctl) {
+  double acc[2][D] = {};
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long v = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double o = __ldg(yold + v * D + k);
+      const double df = __ldg(ynew + v * D + k) - o;
+      acc[0][k] += df * df;
+      acc[1][k] += o * o;
+    }
+  }
+  block_reduce_store<2, D, D>(acc, partials);
+  __shared__ double tot[2][D];
+  if (!grid_reduce_last<2, D>(partials, ctl, tot)) return;
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int j = 0; j < D; ++j) {
+      a += tot[0][j];
+      b += tot[1][j];
+    }
+    ctl->scalar[1] = a;
+    ctl->scalar[2] = b;
+  }
+}
+
+}  // namespace pfe_dev

@@ -1,0 +1,56 @@
+// Host-side launch table: one entry set per embedding dimension D (1..16),
+// each dispatching on the graph topology.  The kernels are instantiated in
+// pfe_kernels_d*.cu so the 16 x 3 template sets compile in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pfe_device.cuh"
+
+namespace pfe_dev {
+struct PcgArgs;
+struct SbArgs;
+}  // namespace pfe_dev
+
+namespace pfe_host {
+
+enum TopoKind : int { kTopoCsr = 0, kTopoGrid1 = 1, kTopoGrid2 = 2 };
+
+struct TopoDesc {
+  int kind = kTopoCsr;
+  pfe_dev::Grid<1> g1{};
+  pfe_dev::Grid<2> g2{};
+  pfe_dev::Csr csr{};
+};
+
+struct Launch {
+  int grid;             // blocks
+  cudaStream_t stream;
+};
+
+struct LaunchTable {
+  int d;
+  void (*pcg_init)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);
+  void (*pcg_spmv)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);
+  void (*pcg_update)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);
+  void (*pcg_finalize)(int n, const double* x0, double* x, pfe_dev::Ctl* ctl, Launch);
+  void (*sb_pass)(const TopoDesc&, const pfe_dev::SbArgs&, Launch);
+  void (*rhs_from_state)(const TopoDesc&, const double* s, const double* b, const double* rq, double* rhs,
+                         double hl, Launch);
+  void (*rhs_quad)(int n, const double* sqd, const double* p, const double* b, double* rq, double hr, Launch);
+  void (*objective)(const TopoDesc&, const double* y, double* partials, pfe_dev::Ctl* ctl, Launch);
+  void (*diff_norms)(int n, const double* ynew, const double* yold, double* partials, pfe_dev::Ctl* ctl, Launch);
+  void (*tsqr_local)(int n, const double* y, const double* sqd, const double* breg, double* rbuf, Launch);
+  void (*tsqr_final)(int nblk, const double* rbuf, double* w, pfe_dev::Ctl* ctl, Launch);
+  void (*project_apply)(int n, const double* y, const double* sqd, double* breg, const double* w, double* p,
+                        double* rq, double hr, Launch);
+  // Largest resident grid (blocks) of the heaviest kernels, for partial sizing.
+  int (*max_blocks_per_sm)();
+};
+
+const LaunchTable& table_for(int d);  // d in [1, 16]
+
+template <int D>
+LaunchTable make_table();
+
+}  // namespace pfe_host

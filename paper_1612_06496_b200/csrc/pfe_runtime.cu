@@ -1,0 +1,1324 @@
+// Host runtime + C ABI of the B200 PFE solver (include/pfe_b200.h).
+//
+// Owns device memory, the operator set-up (sparse.cpp:96-122, pcg.cpp:9-29
+// restated for the device layouts), and the drivers of the nested Bregman
+// loop (solver.cpp:73-136).  The PCG loop runs either host-driven (one
+// control-block read per PCG iteration; needed for callbacks and the
+// relative-change stopping test) or as a CUDA graph whose PCG loop is a
+// device-side conditional WHILE node, so a whole soc / two_stage run is one
+// graph launch with no host round trips.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "pfe_b200.h"
+#include "pfe_errors.h"
+#include "pfe_kernels.cuh"
+#include "pfe_launch.h"
+#include "pfe_polar.cuh"
+
+using pfe_dev::Ctl;
+using pfe_dev::PcgArgs;
+using pfe_dev::SbArgs;
+using pfe_host::Error;
+using pfe_host::LaunchTable;
+using pfe_host::TopoDesc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw Error(PFE_CUDA_ERROR, std::string(#x) + " failed: " + cudaGetErrorString(e_));      \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PFE_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return PFE_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PFE_CUDA_ERROR;
+  }
+}
+
+[[noreturn]] void config_error(const std::string& m) { throw Error(PFE_CONFIG_ERROR, m); }
+
+void require_device(int dev) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    config_error("no CUDA device available: the B200 PFE solver has no CPU fallback");
+  if (dev < 0 || dev >= count) config_error("CUDA device ordinal out of range");
+  cudaDeviceProp prop{};
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10)
+    config_error(std::string("device ") + prop.name + " is not sm_100-class; this library is built for sm_100a only");
+  CK(cudaSetDevice(dev));
+}
+
+// Owner of a set of device allocations.
+struct DevPool {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, cudaStream_t s) {
+    T* d = alloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+  }
+  void release(void* p) {
+    auto it = std::find(ptrs.begin(), ptrs.end(), p);
+    if (it != ptrs.end()) {
+      cudaFree(p);
+      ptrs.erase(it);
+    }
+  }
+  ~DevPool() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+// Per-kernel-class CUDA-event timing (pfe_exec.profile).
+struct Prof {
+  bool on = false;
+  struct Pair {
+    cudaEvent_t a, b;
+    int cls;
+  };
+  std::vector<Pair> pool;
+  size_t used = 0;
+  double ms[PFE_KERNEL_CLASSES] = {};
+  int64_t cnt[PFE_KERNEL_CLASSES] = {};
+  int cur = -1;
+  void begin(int cls, cudaStream_t s) {
+    if (!on) return;
+    if (used == pool.size()) {
+      Pair p{};
+      CK(cudaEventCreate(&p.a));
+      CK(cudaEventCreate(&p.b));
+      pool.push_back(p);
+    }
+    pool[used].cls = cls;
+    CK(cudaEventRecord(pool[used].a, s));
+    cur = static_cast<int>(used);
+  }
+  void end(cudaStream_t s) {
+    if (!on) return;
+    CK(cudaEventRecord(pool[cur].b, s));
+    ++used;
+    if (used >= 4096) collect();
+  }
+  void collect() {
+    if (!on || used == 0) return;
+    CK(cudaEventSynchronize(pool[used - 1].b));
+    for (size_t i = 0; i < used; ++i) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, pool[i].a, pool[i].b));
+      ms[pool[i].cls] += t;
+      cnt[pool[i].cls] += 1;
+    }
+    used = 0;
+  }
+  ~Prof() {
+    for (auto& p : pool) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+  }
+};
+
+// Host bookkeeping of a state that a captured call advances.
+struct Book {
+  double* y;
+  double* y2;
+  int eb_cur;
+  bool inner_zero;
+  bool rq_valid;
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  Book post;    // bookkeeping after the call
+  long inner;   // inner iterations the call runs
+};
+
+struct GraphCache {
+  std::map<std::tuple<int, int, int, int, int, int, int>, GraphEntry> execs;
+  ~GraphCache() {
+    for (auto& kv : execs) cudaGraphExecDestroy(kv.second.exec);
+  }
+};
+
+}  // namespace
+
+// ============================================================== solver ====
+struct pfe_solver {
+  int device = 0;
+  cudaStream_t stream = nullptr, aux = nullptr;
+  int sm = 148;
+  bool use_graphs = true, warn = true;
+  pfe_params prm{};
+  int n = 0;
+  long m = 0;
+  int d = 0;
+  TopoDesc topo;
+  std::vector<long> edge_row;  // edge e -> row of the device edge arrays
+  long edge_rows = 0;
+  DevPool mem;
+  double *deg = nullptr, *sqd = nullptr, *diag = nullptr, *invd = nullptr;
+  Ctl* ctl = nullptr;
+  Ctl* h_ctl = nullptr;  // pinned mirror
+  double* partials = nullptr;
+  int max_grid = 0;
+  double* rbuf = nullptr;
+  int qr_blocks = 1;
+  double* wmat = nullptr;
+  int* log_it = nullptr;
+  int* log_st = nullptr;
+  double* log_rel = nullptr;
+  long log_cap = 0;
+  long inner_launched = 0;  // host mirror of ctl->inner_count
+  const LaunchTable* tab = nullptr;
+  bool jacobi_fallback = false;
+  double setup_s = 0.0;
+  int pred_iters = 1;
+  Prof prof;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;  // device time of the last split_bregman / run_soc / two_stage call
+
+  ~pfe_solver() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (aux) cudaStreamDestroy(aux);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  int grid_for(long threads) const {
+    return static_cast<int>(std::max<long>(1, std::min<long>((threads + pfe_dev::kBlock - 1) / pfe_dev::kBlock, max_grid)));
+  }
+  int tpv() const { return (d == 2 || d == 4 || d == 8 || d == 16) ? d / 2 : 1; }
+  pfe_host::Launch lv() const { return {grid_for(static_cast<long>(n) * tpv()), stream}; }      // vertex kernels
+  pfe_host::Launch le() const { return {grid_for(static_cast<long>(n) * d), stream}; }         // elementwise
+  pfe_host::Launch lr() const { return {grid_for(n), stream}; }                                // row kernels
+
+  void ensure_log(long extra) {
+    const long need = inner_launched + extra;
+    if (need <= log_cap) return;
+    long cap = std::max<long>(need, 2 * log_cap + 256);
+    int* it = mem.alloc<int>(static_cast<size_t>(cap) * d);
+    int* st = mem.alloc<int>(static_cast<size_t>(cap) * d);
+    double* rl = mem.alloc<double>(static_cast<size_t>(cap) * d);
+    if (log_cap > 0) {
+      CK(cudaMemcpyAsync(it, log_it, sizeof(int) * log_cap * d, cudaMemcpyDeviceToDevice, stream));
+      CK(cudaMemcpyAsync(st, log_st, sizeof(int) * log_cap * d, cudaMemcpyDeviceToDevice, stream));
+      CK(cudaMemcpyAsync(rl, log_rel, sizeof(double) * log_cap * d, cudaMemcpyDeviceToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+      mem.release(log_it);
+      mem.release(log_st);
+      mem.release(log_rel);
+    }
+    log_it = it;
+    log_st = st;
+    log_rel = rl;
+    log_cap = cap;
+    struct {
+      int* a;
+      int* b;
+      double* c;
+    } ptrs{it, st, rl};
+    const int capi = static_cast<int>(std::min<long>(cap, 0x7fffffffL));
+    CK(cudaMemcpyAsync(&ctl->log_cap, &capi, sizeof(int), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(&ctl->log_iters, &ptrs, sizeof(ptrs), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  void read_ctl() {
+    CK(cudaMemcpyAsync(h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+};
+
+struct pfe_state {
+  pfe_solver* s = nullptr;
+  DevPool mem;
+  double* ybuf[2] = {nullptr, nullptr};  // the two Y allocations (y / y2 alternate between them)
+  double *y = nullptr, *y2 = nullptr, *p = nullptr, *breg = nullptr, *rq = nullptr, *r = nullptr;
+  double *pb[2] = {nullptr, nullptr}, *q = nullptr;
+  double *eb[2] = {nullptr, nullptr}, *es = nullptr;
+  double* y0 = nullptr;    // device copy of the initial embedding (pfe_state_reset)
+  double* yout = nullptr;  // outer-loop y_old (relative-change test), lazily allocated
+  int eb_cur = 0;
+  bool inner_zero = true;  // split_b == split_s == 0
+  bool rq_valid = false;   // rq == (r/2) sqrt(D) (P - B) for the current P, B
+  GraphCache graphs;
+};
+
+namespace {
+
+// ------------------------------------------------------------- set-up -----
+
+struct HostGraph {
+  int n;
+  long m;
+  const int32_t* ei;
+  const int32_t* ej;
+  const double* w;
+  const double* deg;
+};
+
+// Validation in the reference's order: difference_matrix/csr_from_triplets
+// (sparse.cpp:12-21), form_normal_matrix (98-106), PcgOperator (pcg.cpp:10-12),
+// PfeSolver (solver.cpp:51-57).
+void validate(const HostGraph& g, const pfe_params& p, bool check_solver_caps) {
+  if (g.n < 1) config_error("graph: n must be >= 1");
+  if (g.m < 0) config_error("graph: negative edge count");
+  for (long k = 0; k < g.m; ++k) {
+    const int i = g.ei[k], j = g.ej[k];
+    if (i < 0 || i >= g.n || j < 0 || j >= g.n)
+      config_error("csr_from_triplets: entry (" + std::to_string(k) + "," + std::to_string(i < 0 || i >= g.n ? i : j) +
+                   ") outside " + std::to_string(g.m) + "x" + std::to_string(g.n));
+    if (!std::isfinite(g.w[k])) config_error("csr_from_triplets: non-finite value");
+    if (i >= j) config_error("graph: edge " + std::to_string(k) + " must satisfy i < j (graph.hpp:15-17)");
+  }
+  if (!g.deg) config_error("form_normal_matrix: degree size mismatch");
+  if (p.lambda < 0.0) config_error("form_normal_matrix: lambda must be >= 0");
+  if (p.r <= 0.0) config_error("form_normal_matrix: r must be > 0");
+  for (int v = 0; v < g.n; ++v)
+    if (!(g.deg[v] > 0.0))
+      config_error("form_normal_matrix: nonpositive degree at vertex " + std::to_string(v) + " (isolated vertex)");
+  if (p.pcg_rel_tol <= 0.0) config_error("PcgOperator: rel_tol must be > 0");
+  if (p.pcg_max_iter < 1) config_error("PcgOperator: max_iter must be >= 1");
+  if (p.dim < 1) config_error("PfeSolver: dim must be >= 1");
+  if (p.lambda <= 0.0 || p.r <= 0.0) config_error("PfeSolver: lambda and r must be > 0");
+  if (check_solver_caps && (p.soc_max < 1 || p.sb_max_stage1 < 1))
+    config_error("PfeSolver: iteration caps must be >= 1");
+  if (p.dim > pfe_dev::kMaxD) config_error("PfeSolver: the B200 kernels support dim <= 16");
+  if (p.preconditioner < 0 || p.preconditioner > 2) config_error("PcgConfig: unknown preconditioner");
+}
+
+// Forward stencil slot of edge (i, j) for a W-wide grid of radius R, or -1.
+int grid_slot(int R, int W, int i, int j) {
+  const int yi = i / W, xi = i % W, yj = j / W, xj = j % W;
+  const int dy = yj - yi, dx = xj - xi;
+  if (R == 1) {
+    if (dy == 0 && dx == 1) return 0;
+    if (dy == 1 && dx >= -1 && dx <= 1) return 2 + dx;
+    return -1;
+  }
+  if (dy == 0 && (dx == 1 || dx == 2)) return dx - 1;
+  if (dy == 1 && dx >= -2 && dx <= 2) return 4 + dx;
+  if (dy == 2 && dx >= -2 && dx <= 2) return 9 + dx;
+  return -1;
+}
+
+// Builds the device topology.  Diagonal of A: sum over incident edges in
+// edge order of (hl * w) * w, then + (0.5 r) deg_v last — the accumulation
+// order csr_from_triplets applies to form_normal_matrix's triplets.
+void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad) {
+  const int n = g.n;
+  const long m = g.m;
+  const double hl = 0.5 * S->prm.lambda;
+  const double dterm = 0.5 * S->prm.r;
+  cudaStream_t st = S->stream;
+
+  // incidence lists in increasing edge index (the row order of M^T)
+  std::vector<int> iptr(static_cast<size_t>(n) + 1, 0);
+  for (long k = 0; k < m; ++k) {
+    ++iptr[g.ei[k] + 1];
+    ++iptr[g.ej[k] + 1];
+  }
+  for (int v = 0; v < n; ++v) iptr[v + 1] += iptr[v];
+  std::vector<int> inbr(static_cast<size_t>(2 * m)), ieid(static_cast<size_t>(2 * m));
+  std::vector<double> iw(static_cast<size_t>(2 * m));
+  {
+    std::vector<int> fill(iptr.begin(), iptr.end() - 1);
+    for (long k = 0; k < m; ++k) {
+      const int i = g.ei[k], j = g.ej[k];
+      int at = fill[i]++;
+      inbr[at] = j;
+      ieid[at] = static_cast<int>(k);
+      iw[at] = g.w[k];
+      at = fill[j]++;
+      inbr[at] = i;
+      ieid[at] = static_cast<int>(k);
+      iw[at] = g.w[k];
+    }
+  }
+  std::vector<double> diag(n), invd(n);
+  for (int v = 0; v < n; ++v) {
+    double s = 0.0;
+    for (int k = iptr[v]; k < iptr[v + 1]; ++k) s += (hl * iw[k]) * iw[k];
+    s += dterm * g.deg[v];
+    diag[v] = s;
+    invd[v] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (s > 0.0 ? 1.0 / s : 1.0);
+  }
+  S->diag = S->mem.upload(diag, st);
+  S->invd = S->mem.upload(invd, st);
+
+  // grid eligibility: hint consistent, W wide enough for the slot order to be
+  // the column order, edges strictly lexicographic and all stencil offsets.
+  bool grid = gh > 0 && gw > 0 && static_cast<long>(gh) * gw == n && (grad == 1 || grad == 2) &&
+              gw >= 2 * grad + 2;
+  std::vector<long> slot_of;
+  if (grid) {
+    slot_of.resize(static_cast<size_t>(m));
+    const int S_ = grad == 1 ? 4 : 12;
+    for (long k = 0; k < m && grid; ++k) {
+      if (k > 0 && !(g.ei[k - 1] < g.ei[k] || (g.ei[k - 1] == g.ei[k] && g.ej[k - 1] < g.ej[k]))) grid = false;
+      const int s = grid_slot(grad, gw, g.ei[k], g.ej[k]);
+      if (s < 0) grid = false;
+      slot_of[k] = static_cast<long>(g.ei[k]) * S_ + s;
+    }
+  }
+  if (grid) {
+    const int S_ = grad == 1 ? 4 : 12;
+    std::vector<double> wf(static_cast<size_t>(n) * S_, 0.0);
+    for (long k = 0; k < m; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
+    double* dwf = S->mem.upload(wf, st);
+    S->edge_row = std::move(slot_of);
+    S->edge_rows = static_cast<long>(n) * S_;
+    if (grad == 1) {
+      S->topo.kind = pfe_host::kTopoGrid1;
+      S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd};
+    } else {
+      S->topo.kind = pfe_host::kTopoGrid2;
+      S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd};
+    }
+    return;
+  }
+
+  // General CSR: A rows sorted by column with duplicate columns summed in
+  // edge order (stable sort), exact zeros dropped, diagonal in place.
+  std::vector<int> aptr(static_cast<size_t>(n) + 1, 0), acol;
+  std::vector<double> aval;
+  acol.reserve(static_cast<size_t>(2 * m + n));
+  aval.reserve(static_cast<size_t>(2 * m + n));
+  std::vector<std::pair<int, double>> row;
+  for (int v = 0; v < n; ++v) {
+    row.clear();
+    for (int k = iptr[v]; k < iptr[v + 1]; ++k) row.emplace_back(inbr[k], -((hl * iw[k]) * iw[k]));
+    row.emplace_back(v, diag[v]);
+    std::stable_sort(row.begin(), row.end(),
+                     [](const std::pair<int, double>& a, const std::pair<int, double>& b) { return a.first < b.first; });
+    for (size_t t = 0; t < row.size();) {
+      const int col = row[t].first;
+      double s = 0.0;
+      if (col == v) {
+        s = row[t].second;  // diagonal already accumulated in csr_from_triplets order
+        ++t;
+      } else {
+        for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
+      }
+      if (s != 0.0) {
+        acol.push_back(col);
+        aval.push_back(s);
+      }
+    }
+    aptr[v + 1] = static_cast<int>(acol.size());
+  }
+  S->edge_row.resize(static_cast<size_t>(m));
+  std::iota(S->edge_row.begin(), S->edge_row.end(), 0L);
+  S->edge_rows = m;
+  pfe_dev::Csr c{};
+  c.n = n;
+  c.aptr = S->mem.upload(aptr, st);
+  c.acol = S->mem.upload(acol, st);
+  c.aval = S->mem.upload(aval, st);
+  c.iptr = S->mem.upload(iptr, st);
+  c.inbr = S->mem.upload(inbr, st);
+  c.ieid = S->mem.upload(ieid, st);
+  c.iw = S->mem.upload(iw, st);
+  c.invd = S->invd;
+  S->topo.kind = pfe_host::kTopoCsr;
+  S->topo.csr = c;
+}
+
+void init_common(pfe_solver* S, const pfe_exec* x, int d) {
+  S->device = x ? x->device : 0;
+  require_device(S->device);
+  S->use_graphs = x ? x->use_graphs != 0 : true;
+  S->warn = x ? x->warn != 0 : true;
+  S->prof.on = x ? x->profile != 0 : false;
+  CK(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&S->aux, cudaStreamNonBlocking));
+  CK(cudaDeviceGetAttribute(&S->sm, cudaDevAttrMultiProcessorCount, S->device));
+  S->d = d;
+  S->tab = &pfe_host::table_for(d);
+  S->max_grid = S->sm * S->tab->max_blocks_per_sm();
+  S->partials = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * 3 * pfe_dev::kMaxD);
+  S->ctl = S->mem.alloc<Ctl>(1);
+  CK(cudaMemsetAsync(S->ctl, 0, sizeof(Ctl), S->stream));
+  CK(cudaMallocHost(&S->h_ctl, sizeof(Ctl)));
+  CK(cudaEventCreate(&S->ev0));
+  CK(cudaEventCreate(&S->ev1));
+  std::memset(S->h_ctl, 0, sizeof(Ctl));
+}
+
+// TSQR grid: about 8 tiles of rows per block, at most max_grid blocks.
+int qr_blocks_for(const pfe_solver* S, long n) {
+  const long rows_per_block = 8L * (pfe_dev::kQrRows - S->d);
+  return static_cast<int>(std::max<long>(1, std::min<long>((n + rows_per_block - 1) / rows_per_block, S->max_grid)));
+}
+
+pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exec* x) {
+  if (!g || !p) config_error("null graph or params");
+  const auto t0 = std::chrono::steady_clock::now();
+  HostGraph hg{g->n, static_cast<long>(g->m), g->ei, g->ej, g->w, g->degree};
+  validate(hg, *p, true);
+  if (g->m > 0x3fffffffL) config_error("graph too large for 32-bit edge indices");
+  auto S = std::make_unique<pfe_solver>();
+  S->prm = *p;
+  S->jacobi_fallback = p->preconditioner == PFE_PRECOND_IC0;
+  init_common(S.get(), x, p->dim);
+  S->n = g->n;
+  S->m = g->m;
+  std::vector<double> deg(g->degree, g->degree + g->n), sqd(g->n);
+  for (int v = 0; v < g->n; ++v) sqd[v] = std::sqrt(deg[v]);
+  S->deg = S->mem.upload(deg, S->stream);
+  S->sqd = S->mem.upload(sqd, S->stream);
+  build_topology(S.get(), hg, g->grid_h, g->grid_w, g->grid_radius);
+  S->qr_blocks = qr_blocks_for(S.get(), g->n);
+  S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * S->d * S->d);
+  S->wmat = S->mem.alloc<double>(static_cast<size_t>(S->d) * S->d);
+  S->ensure_log(64);
+  CK(cudaStreamSynchronize(S->stream));
+  S->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return S.release();
+}
+
+// ------------------------------------------------------------- state ------
+
+__global__ void k_colmajor_to_rows(long n, int d, const double* __restrict__ src, double* dst) {
+  const long total = n * d, stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const long v = e / d;
+    const int j = static_cast<int>(e - v * d);
+    dst[e] = src[v + j * n];
+  }
+}
+__global__ void k_rows_to_colmajor(long n, int d, const double* __restrict__ src, double* dst) {
+  const long total = n * d, stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const long v = e % n;
+    const int j = static_cast<int>(e / n);
+    dst[e] = src[v * d + j];
+  }
+}
+__global__ void k_scale_rows(long n, int d, const double* __restrict__ s, const double* __restrict__ y, double* out) {
+  const long total = n * d, stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride)
+    out[e] = s[e / d] * y[e];
+}
+
+// host col-major n x d -> device row-major via a staging buffer
+void upload_rows(pfe_solver* S, const double* host, long n, int d, double* dst, double* staging) {
+  CK(cudaMemcpyAsync(staging, host, sizeof(double) * n * d, cudaMemcpyHostToDevice, S->stream));
+  k_colmajor_to_rows<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, staging, dst);
+  CK(cudaGetLastError());
+}
+void download_rows(pfe_solver* S, const double* src, long n, int d, double* host, double* staging) {
+  k_rows_to_colmajor<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, src, staging);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(host, staging, sizeof(double) * n * d, cudaMemcpyDeviceToHost, S->stream));
+  CK(cudaStreamSynchronize(S->stream));
+}
+
+void state_init_from_y0(pfe_state* st) {
+  pfe_solver* S = st->s;
+  const long nd = static_cast<long>(S->n) * S->d;
+  CK(cudaMemcpyAsync(st->y, st->y0, sizeof(double) * nd, cudaMemcpyDeviceToDevice, S->stream));
+  k_scale_rows<<<S->grid_for(nd), pfe_dev::kBlock, 0, S->stream>>>(S->n, S->d, S->sqd, st->y0, st->p);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(st->breg, 0, sizeof(double) * nd, S->stream));
+  st->inner_zero = true;
+  st->rq_valid = false;
+}
+
+pfe_state* create_state(pfe_solver* S, const double* y0_host) {
+  auto st = std::make_unique<pfe_state>();
+  st->s = S;
+  const size_t nd = static_cast<size_t>(S->n) * S->d;
+  const size_t ed = static_cast<size_t>(S->edge_rows) * S->d;
+  st->y = st->ybuf[0] = st->mem.alloc<double>(nd);
+  st->y2 = st->ybuf[1] = st->mem.alloc<double>(nd);
+  st->p = st->mem.alloc<double>(nd);
+  st->breg = st->mem.alloc<double>(nd);
+  st->rq = st->mem.alloc<double>(nd);
+  st->r = st->mem.alloc<double>(nd);
+  st->pb[0] = st->mem.alloc<double>(nd);
+  st->pb[1] = st->mem.alloc<double>(nd);
+  st->q = st->mem.alloc<double>(nd);
+  st->y0 = st->mem.alloc<double>(nd);
+  st->eb[0] = st->mem.alloc<double>(ed);
+  st->eb[1] = st->mem.alloc<double>(ed);
+  st->es = st->mem.alloc<double>(ed);
+  // absent grid slots must read as exact zeros in every edge array
+  CK(cudaMemsetAsync(st->eb[0], 0, sizeof(double) * ed, S->stream));
+  CK(cudaMemsetAsync(st->eb[1], 0, sizeof(double) * ed, S->stream));
+  CK(cudaMemsetAsync(st->es, 0, sizeof(double) * ed, S->stream));
+  upload_rows(S, y0_host, S->n, S->d, st->y0, st->q);
+  state_init_from_y0(st.get());
+  CK(cudaStreamSynchronize(S->stream));
+  return st.release();
+}
+
+// ------------------------------------------------------------ drivers -----
+
+void check_flags(pfe_solver* S) {
+  S->read_ctl();
+  if (S->h_ctl->nonfinite_y) {
+    CK(cudaMemsetAsync(&S->ctl->nonfinite_y, 0, sizeof(int), S->stream));
+    throw Error(PFE_NUMERICAL_ERROR, "split_bregman: NaN in embedding");
+  }
+  if (S->h_ctl->deficient) {
+    const int def = S->h_ctl->deficient;
+    CK(cudaMemsetAsync(&S->ctl->deficient, 0, sizeof(int), S->stream));
+    throw Error(PFE_NUMERICAL_ERROR,
+                "project_orthogonal: input rank-deficient in " + std::to_string(def) + " column(s)");
+  }
+}
+
+PcgArgs pcg_args(pfe_state* st, const double* rhs) {
+  pfe_solver* S = st->s;
+  PcgArgs a{};
+  a.x0 = st->y;
+  a.x = st->y2;
+  a.rhs = rhs;
+  a.r = st->r;
+  a.pbuf[0] = st->pb[0];
+  a.pbuf[1] = st->pb[1];
+  a.q = st->q;
+  a.ctl = S->ctl;
+  a.partials = S->partials;
+  a.tol = S->prm.pcg_rel_tol;
+  a.max_iter = S->prm.pcg_max_iter;
+  a.use_cond = 0;
+  return a;
+}
+
+void warn_columns(pfe_solver* S) {
+  if (!S->warn) return;
+  for (int j = 0; j < S->d; ++j) {
+    const int stt = S->h_ctl->col[j].status;
+    if (stt == pfe_dev::kMaxIter || stt == pfe_dev::kFailed)
+      std::fprintf(stderr, "pfe: inner solve column %d stopped at rel residual %g\n", j, S->h_ctl->col[j].rel);
+  }
+}
+
+// One PCG solve of all d columns, host-driven: iterations are launched in
+// chunks predicted from the previous solve; kernels of an already finished
+// solve exit immediately, so over-launching is harmless.
+void pcg_solve_host(pfe_state* st, const double* rhs) {
+  pfe_solver* S = st->s;
+  PcgArgs a = pcg_args(st, rhs);
+  const auto L = S->lv();
+  S->prof.begin(0, S->stream);
+  S->tab->pcg_init(S->topo, a, L);
+  S->prof.end(S->stream);
+  int launched = 0;
+  const int maxit = S->prm.pcg_max_iter;
+  while (launched < maxit) {
+    const int chunk = launched == 0 ? std::max(1, std::min(S->pred_iters, maxit)) : 1;
+    for (int c = 0; c < chunk && launched < maxit; ++c, ++launched) {
+      S->prof.begin(1, S->stream);
+      S->tab->pcg_spmv(S->topo, a, L);
+      S->prof.end(S->stream);
+      S->prof.begin(2, S->stream);
+      S->tab->pcg_update(S->topo, a, L);
+      S->prof.end(S->stream);
+    }
+    S->read_ctl();
+    if (!S->h_ctl->any_active) break;
+  }
+  S->pred_iters = std::max(1, S->h_ctl->iter);
+  warn_columns(S);
+  S->prof.begin(3, S->stream);
+  S->tab->pcg_finalize(S->n, st->y, st->y2, S->ctl, S->le());
+  S->prof.end(S->stream);
+  ++S->inner_launched;
+  std::swap(st->y, st->y2);
+}
+
+// The same solve captured into the graph being built on S->stream: init,
+// then a WHILE node whose body is {spmv, update}; the kernels set the loop
+// condition on the device.
+void pcg_solve_captured(pfe_state* st, const double* rhs) {
+  pfe_solver* S = st->s;
+  PcgArgs a = pcg_args(st, rhs);
+  const auto L = S->lv();
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(S->stream, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  a.cond = h;
+  a.use_cond = 1;
+  S->tab->pcg_init(S->topo, a, L);
+  CK(cudaGetLastError());
+  CK(cudaStreamGetCaptureInfo(S->stream, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &np));
+  CK(cudaStreamUpdateCaptureDependencies(S->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(S->aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  S->tab->pcg_spmv(S->topo, a, {L.grid, S->aux});
+  S->tab->pcg_update(S->topo, a, {L.grid, S->aux});
+  CK(cudaGetLastError());
+  CK(cudaStreamEndCapture(S->aux, &body));
+  S->tab->pcg_finalize(S->n, st->y, st->y2, S->ctl, S->le());
+  ++S->inner_launched;
+  std::swap(st->y, st->y2);
+}
+
+struct RunMode {
+  bool captured;
+  pfe_iterate_fn cb;
+  void* user;
+};
+
+void solve_step(pfe_state* st, const double* rhs, const RunMode& mode) {
+  if (mode.captured)
+    pcg_solve_captured(st, rhs);
+  else
+    pcg_solve_host(st, rhs);
+}
+
+// PfeSolver::split_bregman (solver.cpp:73-108).
+void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
+  pfe_solver* S = st->s;
+  const double hl = 0.5 * S->prm.lambda, hr = 0.5 * S->prm.r, gamma = 1.0 / S->prm.lambda;
+  const bool conv = S->prm.conv_tol > 0.0;
+  if (!st->rq_valid) {
+    S->prof.begin(5, S->stream);
+    S->tab->rhs_quad(S->n, S->sqd, st->p, st->breg, st->rq, hr, S->le());
+    S->prof.end(S->stream);
+    st->rq_valid = true;
+  }
+  const double* rhs = st->rq;
+  if (!st->inner_zero) {
+    S->prof.begin(5, S->stream);
+    S->tab->rhs_from_state(S->topo, st->es, st->eb[st->eb_cur], st->rq, st->r, hl, S->lv());
+    S->prof.end(S->stream);
+    rhs = st->r;
+  }
+  for (int it = 0; it < max_iter; ++it) {
+    const bool last = it == max_iter - 1;
+    solve_step(st, rhs, mode);
+    SbArgs sa{};
+    sa.y = st->y;
+    sa.b_old = st->inner_zero ? nullptr : st->eb[st->eb_cur];
+    sa.b_new = st->eb[st->eb_cur ^ 1];
+    sa.s_out = (last || conv || mode.cb) ? st->es : nullptr;
+    sa.rq = st->rq;
+    sa.rhs = last ? nullptr : st->r;
+    sa.hl = hl;
+    sa.gamma = gamma;
+    sa.ctl = S->ctl;
+    S->prof.begin(4, S->stream);
+    S->tab->sb_pass(S->topo, sa, S->lv());
+    S->prof.end(S->stream);
+    st->eb_cur ^= 1;
+    st->inner_zero = false;
+    rhs = st->r;
+    if (mode.cb) {
+      std::vector<double> yh(static_cast<size_t>(S->n) * S->d);
+      download_rows(S, st->y, S->n, S->d, yh.data(), st->q);
+      check_flags(S);
+      mode.cb(it, yh.data(), S->n, S->d, mode.user);
+    }
+    if (conv) {
+      S->tab->diff_norms(S->n, st->y, st->y2, S->partials, S->ctl, S->lr());
+      S->read_ctl();
+      const double den = std::sqrt(S->h_ctl->scalar[2]);
+      if (den > 0.0 && std::sqrt(S->h_ctl->scalar[1]) / den <= S->prm.conv_tol) {
+        if (!last) {
+          // the relative-change test may stop before the last iteration:
+          // rhs for a following call is rebuilt from (s, b)
+        }
+        break;
+      }
+    }
+  }
+}
+
+// Projection + outer Bregman update (solver.cpp:116-118) with the next
+// rhs_quad fused into the same pass.
+void project_step(pfe_state* st) {
+  pfe_solver* S = st->s;
+  S->prof.begin(6, S->stream);
+  S->tab->tsqr_local(S->n, st->y, S->sqd, st->breg, S->rbuf, {S->qr_blocks, S->stream});
+  S->tab->tsqr_final(S->qr_blocks, S->rbuf, S->wmat, S->ctl, {1, S->stream});
+  S->tab->project_apply(S->n, st->y, S->sqd, st->breg, S->wmat, st->p, st->rq, 0.5 * S->prm.r, S->lr());
+  S->prof.end(S->stream);
+  st->rq_valid = true;
+}
+
+// PfeSolver::run_soc (solver.cpp:110-126).
+void run_soc_run(pfe_state* st, int soc_max, int sb_max, const RunMode& mode) {
+  pfe_solver* S = st->s;
+  const bool conv = S->prm.conv_tol > 0.0;
+  const long nd = static_cast<long>(S->n) * S->d;
+  if (conv && !st->yout) st->yout = st->mem.alloc<double>(static_cast<size_t>(nd));
+  for (int k = 0; k < soc_max; ++k) {
+    st->inner_zero = true;
+    if (conv) CK(cudaMemcpyAsync(st->yout, st->y, sizeof(double) * nd, cudaMemcpyDeviceToDevice, S->stream));
+    split_bregman_run(st, sb_max, mode);
+    project_step(st);
+    if (!mode.captured) check_flags(S);
+    if (conv) {
+      S->tab->diff_norms(S->n, st->y, st->yout, S->partials, S->ctl, S->lr());
+      S->read_ctl();
+      const double den = std::sqrt(S->h_ctl->scalar[2]);
+      if (den > 0.0 && std::sqrt(S->h_ctl->scalar[1]) / den <= S->prm.conv_tol) break;
+    }
+  }
+}
+
+// Non-converged-column warnings (solver.cpp:87-92) for iterations run inside a graph.
+void warn_from_log(pfe_solver* S, long lo, long hi) {
+  hi = std::min(hi, S->log_cap);
+  if (hi <= lo) return;
+  const size_t k = static_cast<size_t>(hi - lo) * S->d;
+  std::vector<int> stt(k);
+  std::vector<double> rel(k);
+  CK(cudaMemcpy(stt.data(), S->log_st + lo * S->d, sizeof(int) * k, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rel.data(), S->log_rel + lo * S->d, sizeof(double) * k, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < k; ++i)
+    if (stt[i] == pfe_dev::kMaxIter || stt[i] == pfe_dev::kFailed)
+      std::fprintf(stderr, "pfe: inner solve column %d stopped at rel residual %g\n", static_cast<int>(i % S->d), rel[i]);
+}
+
+enum CallKind { kCallSplit = 0, kCallSoc = 1, kCallTwoStage = 2 };
+
+// Executes a call either host-driven or as one cached CUDA graph.
+void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* user);
+
+// Device time of every call, CUDA events on the solver stream.
+void execute(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* user) {
+  pfe_solver* S = st->s;
+  CK(cudaEventRecord(S->ev0, S->stream));
+  execute_inner(st, kind, a0, a1, cb, user);
+  CK(cudaEventRecord(S->ev1, S->stream));
+  CK(cudaEventSynchronize(S->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+  S->last_ms = ms;
+}
+
+void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* user) {
+  pfe_solver* S = st->s;
+  const bool graphable = S->use_graphs && !cb && !(S->prm.conv_tol > 0.0) && !S->prof.on;
+  long planned = 0;
+  if (kind == kCallSplit) planned = a0;
+  if (kind == kCallSoc) planned = static_cast<long>(a0) * a1;
+  if (kind == kCallTwoStage) planned = static_cast<long>(S->prm.soc_max) * S->prm.sb_max_stage1 + std::max(0, S->prm.sb_max_stage2);
+  S->ensure_log(planned);
+  auto body = [&](const RunMode& mode) {
+    if (kind == kCallSplit) {
+      split_bregman_run(st, a0, mode);
+    } else if (kind == kCallSoc) {
+      run_soc_run(st, a0, a1, mode);
+    } else {
+      run_soc_run(st, S->prm.soc_max, S->prm.sb_max_stage1, mode);
+      if (S->prm.sb_max_stage2 > 0) split_bregman_run(st, S->prm.sb_max_stage2, mode);
+    }
+  };
+  if (!graphable) {
+    body(RunMode{false, cb, user});
+    S->prof.collect();
+    check_flags(S);
+    return;
+  }
+  // graph key: call shape + the state bookkeeping the capture bakes in
+  const auto key = std::make_tuple(kind, a0, a1, st->y == st->ybuf[0] ? 0 : 1, st->eb_cur, st->inner_zero ? 1 : 0,
+                                   st->rq_valid ? 1 : 0);
+  auto it = st->graphs.execs.find(key);
+  if (it == st->graphs.execs.end()) {
+    const Book pre{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
+    const long inner0 = S->inner_launched;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      body(RunMode{true, nullptr, nullptr});
+    } catch (...) {
+      cudaStreamEndCapture(S->stream, &graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(S->stream, &graph));
+    GraphEntry ge{};
+    CK(cudaGraphInstantiate(&ge.exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    ge.post = Book{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
+    ge.inner = S->inner_launched - inner0;
+    st->y = pre.y;
+    st->y2 = pre.y2;
+    st->eb_cur = pre.eb_cur;
+    st->inner_zero = pre.inner_zero;
+    st->rq_valid = pre.rq_valid;
+    S->inner_launched = inner0;
+    it = st->graphs.execs.emplace(key, ge).first;
+  }
+  const long first = S->inner_launched;
+  CK(cudaGraphLaunch(it->second.exec, S->stream));
+  CK(cudaStreamSynchronize(S->stream));
+  const GraphEntry& ge = it->second;
+  st->y = ge.post.y;
+  st->y2 = ge.post.y2;
+  st->eb_cur = ge.post.eb_cur;
+  st->inner_zero = ge.post.inner_zero;
+  st->rq_valid = ge.post.rq_valid;
+  S->inner_launched += ge.inner;
+  if (S->warn) warn_from_log(S, first, S->inner_launched);
+  check_flags(S);
+}
+
+}  // namespace
+
+// ================================================================ C ABI ===
+extern "C" {
+
+const char* pfe_last_error(void) { return g_last_error.c_str(); }
+
+pfe_params pfe_params_default(void) {
+  pfe_params p{};
+  p.dim = 5;
+  p.lambda = 100.0;
+  p.r = 1.0;
+  p.soc_max = 10;
+  p.sb_max_stage1 = 5;
+  p.sb_max_stage2 = 100;
+  p.conv_tol = 1e-4;
+  p.pcg_rel_tol = 1e-6;
+  p.pcg_max_iter = 1000;
+  p.preconditioner = PFE_PRECOND_IC0;
+  return p;
+}
+
+pfe_exec pfe_exec_default(void) {
+  pfe_exec x{};
+  x.device = 0;
+  x.use_graphs = 1;
+  x.warn = 1;
+  x.profile = 0;
+  return x;
+}
+
+int pfe_device_check(int32_t device) {
+  return guarded([&] { require_device(device); });
+}
+
+int pfe_solver_create(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, pfe_solver** out) {
+  return guarded([&] { *out = create_solver(g, p, x); });
+}
+
+void pfe_solver_destroy(pfe_solver* s) { delete s; }
+
+int pfe_solver_report(const pfe_solver* s, pfe_report* out) {
+  return guarded([&] {
+    pfe_report r{};
+    r.topology = s->topo.kind;
+    r.n = s->n;
+    r.m = s->m;
+    r.d = s->d;
+    r.jacobi_fallback = s->jacobi_fallback ? 1 : 0;
+    r.setup_seconds = s->setup_s;
+    const long cnt = std::min(s->inner_launched, s->log_cap);
+    std::vector<int> it(static_cast<size_t>(cnt) * s->d), stt(static_cast<size_t>(cnt) * s->d);
+    if (cnt > 0) {
+      CK(cudaMemcpy(it.data(), s->log_it, sizeof(int) * it.size(), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(stt.data(), s->log_st, sizeof(int) * stt.size(), cudaMemcpyDeviceToHost));
+    }
+    r.inner_iterations = cnt;
+    for (long i = 0; i < cnt; ++i) {
+      int mx = 0;
+      for (int j = 0; j < s->d; ++j) {
+        const int v = it[static_cast<size_t>(i) * s->d + j], st = stt[static_cast<size_t>(i) * s->d + j];
+        mx = std::max(mx, v);
+        r.pcg_column_iterations += v;
+        if (st == pfe_dev::kMaxIter || st == pfe_dev::kFailed) ++r.nonconverged;
+        if (st == pfe_dev::kFailed) ++r.failed;
+      }
+      r.pcg_iterations += mx;
+    }
+    *out = r;
+  });
+}
+
+int64_t pfe_solver_pcg_log(const pfe_solver* s, int32_t* iters, int32_t* status, double* rel, int64_t cap) {
+  int64_t cnt = 0;
+  const int rc = guarded([&] {
+    cnt = std::min<int64_t>(std::min(s->inner_launched, s->log_cap), cap);
+    if (cnt <= 0) return;
+    const size_t k = static_cast<size_t>(cnt) * s->d;
+    if (iters) CK(cudaMemcpy(iters, s->log_it, sizeof(int) * k, cudaMemcpyDeviceToHost));
+    if (status) CK(cudaMemcpy(status, s->log_st, sizeof(int) * k, cudaMemcpyDeviceToHost));
+    if (rel) CK(cudaMemcpy(rel, s->log_rel, sizeof(double) * k, cudaMemcpyDeviceToHost));
+  });
+  return rc == PFE_OK ? cnt : -rc;
+}
+
+int pfe_solver_kernel_times(const pfe_solver* s, pfe_kernel_times* out, int reset) {
+  return guarded([&] {
+    auto* S = const_cast<pfe_solver*>(s);
+    S->prof.collect();
+    for (int i = 0; i < PFE_KERNEL_CLASSES; ++i) {
+      out->ms[i] = S->prof.ms[i];
+      out->launches[i] = S->prof.cnt[i];
+      if (reset) {
+        S->prof.ms[i] = 0.0;
+        S->prof.cnt[i] = 0;
+      }
+    }
+  });
+}
+
+double pfe_solver_last_ms(const pfe_solver* s) { return s ? s->last_ms : -1.0; }
+
+int pfe_state_create(pfe_solver* s, const double* y0, pfe_state** out) {
+  return guarded([&] {
+    if (!y0) config_error("PfeSolver: initial embedding has wrong shape");
+    CK(cudaSetDevice(s->device));
+    *out = create_state(s, y0);
+  });
+}
+
+int pfe_state_reset(pfe_state* st) {
+  return guarded([&] {
+    CK(cudaSetDevice(st->s->device));
+    state_init_from_y0(st);
+  });
+}
+
+void pfe_state_destroy(pfe_state* st) { delete st; }
+
+int pfe_state_get(pfe_state* st, int32_t field, double* out) {
+  return guarded([&] {
+    pfe_solver* S = st->s;
+    CK(cudaSetDevice(S->device));
+    const int d = S->d;
+    if (field <= PFE_FIELD_BREGMAN) {
+      const double* src = field == PFE_FIELD_Y ? st->y : (field == PFE_FIELD_P ? st->p : st->breg);
+      download_rows(S, src, S->n, d, out, st->q);
+      return;
+    }
+    if (field != PFE_FIELD_SPLIT_B && field != PFE_FIELD_SPLIT_S) config_error("pfe_state_get: unknown field");
+    const long m = S->m;
+    if (st->inner_zero) {
+      std::fill(out, out + m * d, 0.0);
+      return;
+    }
+    const double* src = field == PFE_FIELD_SPLIT_B ? st->eb[st->eb_cur] : st->es;
+    std::vector<double> rows(static_cast<size_t>(S->edge_rows) * d);
+    CK(cudaMemcpy(rows.data(), src, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost));
+    for (long e = 0; e < m; ++e)
+      for (int j = 0; j < d; ++j) out[e + j * m] = rows[static_cast<size_t>(S->edge_row[e]) * d + j];
+  });
+}
+
+int pfe_state_set(pfe_state* st, int32_t field, const double* in) {
+  return guarded([&] {
+    pfe_solver* S = st->s;
+    CK(cudaSetDevice(S->device));
+    const int d = S->d;
+    if (field <= PFE_FIELD_BREGMAN) {
+      double* dst = field == PFE_FIELD_Y ? st->y : (field == PFE_FIELD_P ? st->p : st->breg);
+      upload_rows(S, in, S->n, d, dst, st->q);
+      CK(cudaStreamSynchronize(S->stream));
+      if (field != PFE_FIELD_Y) st->rq_valid = false;
+      return;
+    }
+    if (field != PFE_FIELD_SPLIT_B && field != PFE_FIELD_SPLIT_S) config_error("pfe_state_set: unknown field");
+    const long m = S->m;
+    // materialize both edge arrays before a partial update of one of them
+    std::vector<double> b_rows(static_cast<size_t>(S->edge_rows) * d, 0.0), s_rows(b_rows.size(), 0.0);
+    if (!st->inner_zero) {
+      CK(cudaMemcpy(b_rows.data(), st->eb[st->eb_cur], sizeof(double) * b_rows.size(), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(s_rows.data(), st->es, sizeof(double) * s_rows.size(), cudaMemcpyDeviceToHost));
+    }
+    std::vector<double>& tgt = field == PFE_FIELD_SPLIT_B ? b_rows : s_rows;
+    for (long e = 0; e < m; ++e)
+      for (int j = 0; j < d; ++j) tgt[static_cast<size_t>(S->edge_row[e]) * d + j] = in[e + j * m];
+    CK(cudaMemcpy(st->eb[st->eb_cur], b_rows.data(), sizeof(double) * b_rows.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(st->es, s_rows.data(), sizeof(double) * s_rows.size(), cudaMemcpyHostToDevice));
+    st->inner_zero = false;
+  });
+}
+
+int pfe_split_bregman(pfe_solver* s, pfe_state* st, int32_t max_iter, pfe_iterate_fn cb, void* user) {
+  return guarded([&] {
+    CK(cudaSetDevice(s->device));
+    if (max_iter <= 0) return;
+    execute(st, kCallSplit, max_iter, 0, cb, user);
+  });
+}
+
+int pfe_run_soc(pfe_solver* s, pfe_state* st, int32_t soc_max, int32_t sb_max) {
+  return guarded([&] {
+    CK(cudaSetDevice(s->device));
+    if (soc_max <= 0) return;
+    execute(st, kCallSoc, soc_max, std::max(0, sb_max), nullptr, nullptr);
+  });
+}
+
+int pfe_two_stage(pfe_solver* s, pfe_state* st) {
+  return guarded([&] {
+    CK(cudaSetDevice(s->device));
+    execute(st, kCallTwoStage, 0, 0, nullptr, nullptr);
+  });
+}
+
+int pfe_state_objective(pfe_solver* s, pfe_state* st, double* out) {
+  return guarded([&] {
+    CK(cudaSetDevice(s->device));
+    s->tab->objective(s->topo, st->y, s->partials, s->ctl, s->lv());
+    CK(cudaGetLastError());
+    s->read_ctl();
+    *out = s->h_ctl->scalar[0];
+  });
+}
+
+int pfe_solve(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t mode, const double* y0,
+              double* y_out, pfe_report* rep) {
+  return guarded([&] {
+    std::unique_ptr<pfe_solver> S(create_solver(g, p, x));
+    std::unique_ptr<pfe_state> st(create_state(S.get(), y0));
+    if (mode == 1)
+      execute(st.get(), kCallTwoStage, 0, 0, nullptr, nullptr);
+    else
+      execute(st.get(), kCallSoc, p->soc_max, p->sb_max_stage1, nullptr, nullptr);
+    download_rows(S.get(), st->y, S->n, S->d, y_out, st->q);
+    if (rep && pfe_solver_report(S.get(), rep) != PFE_OK) throw Error(PFE_CUDA_ERROR, g_last_error);
+  });
+}
+
+int pfe_split_bregman_standalone(const pfe_graph* g, const double* p, const double* b, const pfe_params* prm,
+                                 int32_t d, const double* y_init, int32_t max_iter, const pfe_exec* x,
+                                 double* y_out, pfe_iterate_fn cb, void* user) {
+  return guarded([&] {
+    if (!prm) config_error("null params");
+    pfe_params local = *prm;
+    local.dim = d;  // solver.cpp:142-143
+    HostGraph hg{g->n, static_cast<long>(g->m), g->ei, g->ej, g->w, g->degree};
+    validate(hg, local, false);
+    auto S = std::make_unique<pfe_solver>();
+    S->prm = local;
+    S->warn = false;  // the standalone entry point does not warn (solver.cpp:161-180)
+    S->jacobi_fallback = local.preconditioner == PFE_PRECOND_IC0;
+    init_common(S.get(), x, d);
+    S->warn = false;
+    S->n = g->n;
+    S->m = g->m;
+    std::vector<double> deg(g->degree, g->degree + g->n), sqd(g->n);
+    for (int v = 0; v < g->n; ++v) sqd[v] = std::sqrt(deg[v]);
+    S->deg = S->mem.upload(deg, S->stream);
+    S->sqd = S->mem.upload(sqd, S->stream);
+    build_topology(S.get(), hg, g->grid_h, g->grid_w, g->grid_radius);
+    S->qr_blocks = 1;
+    S->rbuf = S->mem.alloc<double>(static_cast<size_t>(d) * d);
+    S->wmat = S->mem.alloc<double>(static_cast<size_t>(d) * d);
+    std::unique_ptr<pfe_state> st(create_state(S.get(), y_init));
+    upload_rows(S.get(), p, S->n, d, st->p, st->q);
+    upload_rows(S.get(), b, S->n, d, st->breg, st->q);
+    st->rq_valid = false;
+    if (max_iter > 0) execute(st.get(), kCallSplit, max_iter, 0, cb, user);
+    download_rows(S.get(), st->y, S->n, d, y_out, st->q);
+  });
+}
+
+int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, const double* values, int32_t d,
+                        const double* b, const double* x0, double rel_tol, int32_t max_iter, int32_t preconditioner,
+                        const pfe_exec* x, double* x_out, int32_t* iterations, int32_t* converged, double* residual,
+                        int32_t* jacobi_fallback) {
+  return guarded([&] {
+    if (rel_tol <= 0.0) config_error("PcgOperator: rel_tol must be > 0");
+    if (max_iter < 1) config_error("PcgOperator: max_iter must be >= 1");
+    if (n < 1 || d < 1 || d > pfe_dev::kMaxD) config_error("pcg_solve_multi: dimension mismatch");
+    auto S = std::make_unique<pfe_solver>();
+    S->prm = pfe_params_default();
+    S->prm.dim = d;
+    S->prm.pcg_rel_tol = rel_tol;
+    S->prm.pcg_max_iter = max_iter;
+    S->prm.preconditioner = preconditioner;
+    S->warn = false;
+    init_common(S.get(), x, d);
+    S->warn = false;
+    S->n = n;
+    S->m = 0;
+    const int nnz = row_ptr[n];
+    std::vector<int> aptr(row_ptr, row_ptr + n + 1), acol(col_idx, col_idx + nnz);
+    std::vector<double> aval(values, values + nnz), invd(n, 1.0);
+    if (preconditioner != PFE_PRECOND_NONE)
+      for (int r = 0; r < n; ++r)
+        for (int k = aptr[r]; k < aptr[r + 1]; ++k)
+          if (acol[k] == r && aval[k] > 0.0) invd[r] = 1.0 / aval[k];  // pcg.cpp:15-20
+    pfe_dev::Csr c{};
+    c.n = n;
+    c.aptr = S->mem.upload(aptr, S->stream);
+    c.acol = S->mem.upload(acol, S->stream);
+    c.aval = S->mem.upload(aval, S->stream);
+    c.invd = S->mem.upload(invd, S->stream);
+    S->topo.kind = pfe_host::kTopoCsr;
+    S->topo.csr = c;
+    S->edge_rows = 0;
+    std::unique_ptr<pfe_state> st(create_state(S.get(), x0));
+    upload_rows(S.get(), b, n, d, st->r, st->q);
+    S->ensure_log(1);
+    pcg_solve_host(st.get(), st->r);
+    download_rows(S.get(), st->y, n, d, x_out, st->q);
+    S->read_ctl();
+    for (int j = 0; j < d; ++j) {
+      const auto& col = S->h_ctl->col[j];
+      const bool ok = col.status == pfe_dev::kConverged || col.status == pfe_dev::kConvInit ||
+                      col.status == pfe_dev::kZeroRhs;
+      if (iterations) iterations[j] = col.iters;
+      if (converged) converged[j] = ok ? 1 : 0;
+      if (residual) residual[j] = col.rel;
+      if (jacobi_fallback) jacobi_fallback[j] = preconditioner == PFE_PRECOND_IC0 ? 1 : 0;
+    }
+  });
+}
+
+int pfe_objective(const pfe_graph* g, int32_t d, const double* y, const pfe_exec* x, double* out) {
+  return guarded([&] {
+    pfe_params p = pfe_params_default();
+    p.dim = d;
+    p.lambda = 2.0;  // operator unused; any valid values
+    std::vector<double> unit;
+    pfe_graph gg = *g;
+    if (!gg.degree) {
+      unit.assign(g->n, 1.0);
+      gg.degree = unit.data();
+    }
+    HostGraph hg{gg.n, static_cast<long>(gg.m), gg.ei, gg.ej, gg.w, gg.degree};
+    if (gg.n < 1) config_error("objective: dimension mismatch");
+    for (long k = 0; k < hg.m; ++k) {
+      if (hg.ei[k] < 0 || hg.ei[k] >= hg.n || hg.ej[k] < 0 || hg.ej[k] >= hg.n || hg.ei[k] >= hg.ej[k])
+        config_error("objective: invalid edge " + std::to_string(k));
+    }
+    auto S = std::make_unique<pfe_solver>();
+    S->prm = p;
+    init_common(S.get(), x, d);
+    S->n = gg.n;
+    S->m = gg.m;
+    build_topology(S.get(), hg, gg.grid_h, gg.grid_w, gg.grid_radius);
+    double* dy = S->mem.alloc<double>(static_cast<size_t>(gg.n) * d);
+    double* stg = S->mem.alloc<double>(static_cast<size_t>(gg.n) * d);
+    upload_rows(S.get(), y, gg.n, d, dy, stg);
+    S->tab->objective(S->topo, dy, S->partials, S->ctl, S->lv());
+    CK(cudaGetLastError());
+    S->read_ctl();
+    *out = S->h_ctl->scalar[0];
+  });
+}
+
+}  // extern "C"
+
+__global__ void k_shrink(long count, const double* __restrict__ v, double gamma, double* out) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += stride)
+    out[e] = pfe_dev::shrink1(v[e], gamma);
+}
+
+extern "C" {
+
+int pfe_shrink(int64_t count, const double* v, double gamma, const pfe_exec* x, double* out) {
+  return guarded([&] {
+    if (gamma < 0.0) config_error("shrink: gamma must be >= 0");
+    require_device(x ? x->device : 0);
+    if (count <= 0) return;
+    double *dv = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dv, sizeof(double) * count));
+    CK(cudaMalloc(&dout, sizeof(double) * count));
+    CK(cudaMemcpy(dv, v, sizeof(double) * count, cudaMemcpyHostToDevice));
+    k_shrink<<<static_cast<int>(std::min<int64_t>((count + 255) / 256, 4096)), 256>>>(count, dv, gamma, dout);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost);
+    cudaFree(dv);
+    cudaFree(dout);
+    CK(e);
+  });
+}
+
+int pfe_project_orthogonal(int32_t n, int32_t d, const double* a, const pfe_exec* x, double* p_out) {
+  return guarded([&] {
+    if (n < d) config_error("project_orthogonal: need rows >= cols");
+    if (d < 1 || d > pfe_dev::kMaxD) config_error("project_orthogonal: the B200 kernels support 1 <= cols <= 16");
+    auto S = std::make_unique<pfe_solver>();
+    init_common(S.get(), x, d);
+    S->n = n;
+    const int blocks = qr_blocks_for(S.get(), n);
+    double* da = S->mem.alloc<double>(static_cast<size_t>(n) * d);
+    double* stg = S->mem.alloc<double>(static_cast<size_t>(n) * d);
+    double* dp = S->mem.alloc<double>(static_cast<size_t>(n) * d);
+    double* rb = S->mem.alloc<double>(static_cast<size_t>(blocks) * d * d);
+    double* w = S->mem.alloc<double>(static_cast<size_t>(d) * d);
+    upload_rows(S.get(), a, n, d, da, stg);
+    S->tab->tsqr_local(n, da, nullptr, nullptr, rb, {blocks, S->stream});
+    S->tab->tsqr_final(blocks, rb, w, S->ctl, {1, S->stream});
+    S->tab->project_apply(n, da, nullptr, nullptr, w, dp, nullptr, 0.0, S->lr());
+    CK(cudaGetLastError());
+    check_flags(S.get());
+    download_rows(S.get(), dp, n, d, p_out, stg);
+  });
+}
+
+int pfe_d_orthonormalize(int32_t n, int32_t d, const double* a, const double* degree, double* out) {
+  return guarded([&] { pfe_host::d_orthonormalize(n, d, a, degree, out); });
+}
+
+int pfe_random_embedding(int32_t n, int32_t d, uint64_t seed, const double* degree, double* out) {
+  return guarded([&] { pfe_host::random_embedding(n, d, seed, degree, out); });
+}
+
+int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
+               int32_t* labels) {
+  return guarded([&] { pfe_host::kmeans(n, d, points, k, seed, max_iter, labels); });
+}
+
+}  // extern "C"
+
+namespace pfe_host {
+const LaunchTable& table_for(int d) {
+  static const LaunchTable tables[16] = {
+      make_table<1>(),  make_table<2>(),  make_table<3>(),  make_table<4>(),  make_table<5>(),  make_table<6>(),
+      make_table<7>(),  make_table<8>(),  make_table<9>(),  make_table<10>(), make_table<11>(), make_table<12>(),
+      make_table<13>(), make_table<14>(), make_table<15>(), make_table<16>()};
+  if (d < 1 || d > 16) throw Error(PFE_CONFIG_ERROR, "embedding dimension must be in [1, 16]");
+  return tables[d - 1];
+}
+}  // namespace pfe_host
