@@ -555,8 +555,12 @@ void state_init_from_y0(pfe_state* st) {
   pfe_solver* S = st->s;
   const long nd = static_cast<long>(S->n) * S->d;
   CK(cudaMemcpyAsync(st->y, st->y0, sizeof(double) * nd, cudaMemcpyDeviceToDevice, S->stream));
-  k_scale_rows<<<S->grid_for(nd), pfe_dev::kBlock, 0, S->stream>>>(S->n, S->d, S->sqd, st->y0, st->p);
-  CK(cudaGetLastError());
+  if (S->sqd) {
+    k_scale_rows<<<S->grid_for(nd), pfe_dev::kBlock, 0, S->stream>>>(S->n, S->d, S->sqd, st->y0, st->p);
+    CK(cudaGetLastError());
+  } else {  // operator-only solvers (pfe_pcg_solve_multi) have no degree vector
+    CK(cudaMemsetAsync(st->p, 0, sizeof(double) * nd, S->stream));
+  }
   CK(cudaMemsetAsync(st->breg, 0, sizeof(double) * nd, S->stream));
   st->inner_zero = true;
   st->rq_valid = false;
