@@ -247,10 +247,10 @@ struct Csr {
 // combined in fixed order through shared memory; block b writes
 // partials[b][NQ][D].  The last block to finish (ticket) reduces the block
 // partials in a fixed order and runs the scalar epilogue.
-template <int NQ, int D, int V>
+template <int NQ, int D, int V, int NT = kBlock>
 __device__ __forceinline__ void block_reduce_store(double (&acc)[NQ][V], double* __restrict__ partials) {
   constexpr int TPV = D / V;
-  __shared__ double red[kBlock / 32][NQ][D];
+  __shared__ double red[NT / 32][NQ][D];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o >= TPV; o >>= 1) {
@@ -270,16 +270,22 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NQ][V], double*
     const int q = threadIdx.x / D, c = threadIdx.x - q * D;
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kBlock / 32; ++w) s += red[w][q][c];
-    partials[(static_cast<long>(blockIdx.x) * NQ + q) * D + c] = s;
+    for (int w = 0; w < NT / 32; ++w) s += red[w][q][c];
+    partials[static_cast<long>(q * D + c) * gridDim.x + blockIdx.x] = s;  // pair-major
   }
 }
 
 // Returns true in exactly one block (the last to arrive); that block's
-// shared `out[NQ][D]` then holds the grid totals.
-template <int NQ, int D>
+// shared `out[NQ][D]` then holds the grid totals.  The final reduction uses
+// every thread of the last block: thread t owns blocks t, t+256, ... of each
+// (quantity, column) pair (coalesced: partials are stored pair-major), then a
+// warp butterfly and a fixed-order sum over warps — deterministic.
+template <int NQ, int D, int NT = kBlock>
 __device__ __forceinline__ bool grid_reduce_last(const double* partials, Ctl* ctl, double (&out)[NQ][D]) {
+  constexpr int P = NQ * D;
+  constexpr int CH = P < 16 ? P : 16;  // pairs reduced per pass
   __shared__ bool last;
+  __shared__ double wsum[NT / 32][CH];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -291,14 +297,32 @@ __device__ __forceinline__ bool grid_reduce_last(const double* partials, Ctl* ct
   __threadfence();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
-  for (int pair = warp; pair < NQ * D; pair += kBlock / 32) {
-    double s = 0.0;
-    for (int b = lane; b < nb; b += 32) s += __ldcg(partials + static_cast<long>(b) * NQ * D + pair);
+  for (int base = 0; base < P; base += CH) {
+    double acc[CH];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[pair / D][pair % D] = s;
+    for (int k = 0; k < CH; ++k) acc[k] = 0.0;
+    for (int b = threadIdx.x; b < nb; b += NT) {
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (base + k < P) acc[k] += __ldcg(partials + static_cast<long>(base + k) * nb + b);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < CH; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < CH; ++k) wsum[warp][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < CH && base + threadIdx.x < P) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) s += wsum[w][threadIdx.x];
+      const int pr = base + threadIdx.x;
+      out[pr / D][pr % D] = s;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (threadIdx.x == 0) ctl->ticket = 0;
   return true;
 }

@@ -32,7 +32,114 @@ struct PcgArgs {
   int max_iter;
   cudaGraphConditionalHandle cond;  // loop handle when running inside a graph
   int use_cond;
+  // Iteration parity, fixed per launch so no buffer address depends on the
+  // device control block: 0 = first iteration (p from init in pbuf[0],
+  // x read from x0), 1 = odd iteration >= 3 (p' -> pbuf[0], p_old = pbuf[1]),
+  // 2 = even iteration (p' -> pbuf[1], p_old = pbuf[0]).
+  int phase;
 };
+
+__host__ __device__ __forceinline__ int pcg_phase(int it) { return it == 1 ? 0 : ((it & 1) ? 1 : 2); }
+__device__ __forceinline__ double* pcg_pnew(const PcgArgs& a) { return a.phase == 2 ? a.pbuf[1] : a.pbuf[0]; }
+__device__ __forceinline__ const double* pcg_pold(const PcgArgs& a) { return a.phase == 1 ? a.pbuf[1] : a.pbuf[0]; }
+
+// Scalar epilogues, run by warp 0 of the last block (see grid_reduce_last):
+// lane j owns column j, loads its PcgCol once, updates it in registers and
+// writes it back, so the epilogue costs one control-block round trip instead
+// of a dependent chain per field.
+constexpr double kInf = __builtin_huge_val();
+
+template <int D, int NQ>
+__device__ __forceinline__ void pcg_init_epilogue(const PcgArgs& a, const double (&tot)[NQ][D]) {
+  const int j = threadIdx.x;
+  bool act = false, fix = false;
+  if (j < D) {
+    PcgCol col{};
+    col.bnorm = sqrt(tot[0][j]);
+    if (col.bnorm == 0.0) {
+      col.status = kZeroRhs;
+      col.rel = 0.0;
+    } else {
+      col.rel = sqrt(tot[1][j]) / col.bnorm;
+      if (col.rel <= a.tol) {
+        col.status = kConvInit;
+      } else {
+        col.status = kActive;
+        col.rz = tot[2][j];
+      }
+    }
+    act = col.status == kActive;
+    fix = !act;
+    a.ctl->col[j] = col;
+  }
+  const bool any = __any_sync(0xffffffffu, act), anyfix = __any_sync(0xffffffffu, fix);
+  if (j == 0) {
+    a.ctl->iter = 0;
+    a.ctl->any_active = any;
+    a.ctl->need_fix = anyfix;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
+  }
+}
+
+template <int D, int NQ>
+__device__ __forceinline__ void pcg_spmv_epilogue(const PcgArgs& a, const double (&tot)[NQ][D]) {
+  const int j = threadIdx.x;
+  bool failed = false;
+  if (j < D) {
+    PcgCol col = a.ctl->col[j];
+    if (col.status == kActive) {
+      const double pq = tot[0][j];
+      col.pq = pq;
+      if (!(pq > 0.0) || !isfinite(pq)) {  // pcg.cpp:71-72
+        col.status = kFailed;
+        col.iters = 0;
+        col.rel = kInf;
+        failed = true;
+      } else {
+        col.alpha = col.rz / pq;
+      }
+      a.ctl->col[j] = col;
+    }
+  }
+  if (__any_sync(0xffffffffu, failed) && j == 0) a.ctl->need_fix = 1;
+}
+
+template <int D, int NQ>
+__device__ __forceinline__ void pcg_update_epilogue(const PcgArgs& a, const double (&tot)[NQ][D], int it) {
+  const int j = threadIdx.x;
+  bool act = false, failed = false;
+  if (j < D) {
+    PcgCol col = a.ctl->col[j];
+    if (col.status == kActive) {
+      if (tot[2][j] > 0.0) {  // pcg.cpp:75
+        col.status = kFailed;
+        col.iters = 0;
+        col.rel = kInf;
+        failed = true;
+      } else {
+        col.rel = sqrt(tot[0][j]) / col.bnorm;
+        col.iters = it;
+        if (col.rel <= a.tol) {
+          col.status = kConverged;
+        } else if (it >= a.max_iter) {
+          col.status = kMaxIter;
+        } else {
+          col.beta = tot[1][j] / col.rz;
+          col.rz = tot[1][j];
+          act = true;
+        }
+      }
+      a.ctl->col[j] = col;
+    }
+  }
+  const bool any = __any_sync(0xffffffffu, act), anyfail = __any_sync(0xffffffffu, failed);
+  if (j == 0) {
+    a.ctl->iter = it;
+    a.ctl->any_active = any;
+    if (anyfail) a.ctl->need_fix = 1;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
+  }
+}
 
 // ---------------------------------------------------------------- PCG init --
 template <int D, class Topo>
@@ -67,34 +174,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
   block_reduce_store<3, D, V>(acc, a.partials);
   __shared__ double tot[3][D];
   if (!grid_reduce_last<3, D>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x == 0) {
-    Ctl* c = a.ctl;
-    int any = 0, fix = 0;
-    for (int j = 0; j < D; ++j) {
-      PcgCol& col = c->col[j];
-      col.bnorm = sqrt(tot[0][j]);
-      col.iters = 0;
-      col.alpha = col.beta = col.pq = 0.0;
-      if (col.bnorm == 0.0) {
-        col.status = kZeroRhs;
-        col.rel = 0.0;
-      } else {
-        col.rel = sqrt(tot[1][j]) / col.bnorm;
-        if (col.rel <= a.tol) {
-          col.status = kConvInit;
-        } else {
-          col.status = kActive;
-          col.rz = tot[2][j];
-        }
-      }
-      any |= (col.status == kActive);
-      fix |= (col.status != kActive);
-    }
-    c->iter = 0;
-    c->any_active = any;
-    c->need_fix = fix;
-    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
-  }
+  if (threadIdx.x < 32) pcg_init_epilogue<D>(a, tot);
 }
 
 // ------------------------------------------------------- PCG SpMV (+ p update)
@@ -103,13 +183,13 @@ __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   const Ctl* c = a.ctl;
   if (!c->any_active) return;
-  const int it = c->iter + 1;
+  const bool first = a.phase == 0;
   const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
   double beta[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) beta[k] = (c->col[gfirst + k].status == kActive) ? c->col[gfirst + k].beta : 0.0;
-  double* pnew = (it & 1) ? a.pbuf[0] : a.pbuf[1];
-  const double* pold = (it & 1) ? a.pbuf[1] : a.pbuf[0];
+  double* pnew = pcg_pnew(a);
+  const double* pold = pcg_pold(a);
   double acc[1][V] = {};
   const long total = static_cast<long>(topo.n) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
@@ -118,7 +198,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double q[V] = {};
     Row<V> pv;
-    if (it == 1) {
+    if (first) {
       pv = ldg_row<V>(pnew + static_cast<long>(v) * D + c0);
       topo.visitA(v, [&](int u, double av) {
         const Row<V> pu = ldg_row<V>(pnew + static_cast<long>(u) * D + c0);
@@ -156,23 +236,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
   block_reduce_store<1, D, V>(acc, a.partials);
   __shared__ double tot[1][D];
   if (!grid_reduce_last<1, D>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x == 0) {
-    Ctl* cw = a.ctl;
-    for (int j = 0; j < D; ++j) {
-      PcgCol& col = cw->col[j];
-      if (col.status != kActive) continue;
-      const double pq = tot[0][j];
-      col.pq = pq;
-      if (!(pq > 0.0) || !isfinite(pq)) {  // pcg.cpp:71-72
-        col.status = kFailed;
-        col.iters = 0;
-        col.rel = __longlong_as_double(0x7ff0000000000000ll);
-        cw->need_fix = 1;
-      } else {
-        col.alpha = col.rz / pq;
-      }
-    }
-  }
+  if (threadIdx.x < 32) pcg_spmv_epilogue<D>(a, tot);
 }
 
 // ----------------------------------------------------------- PCG update -----
@@ -180,21 +244,23 @@ template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   const Ctl* c = a.ctl;
-  if (!c->any_active) return;
-  const int it = c->iter + 1;
   const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
+  // Control values and the first item's data are loaded together: no
+  // control-block round trip precedes the data loads.
+  const int active = c->any_active;
   double alpha[V];
   bool act[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     act[k] = c->col[gfirst + k].status == kActive;
-    alpha[k] = act[k] ? c->col[gfirst + k].alpha : 0.0;
+    alpha[k] = c->col[gfirst + k].alpha;
   }
-  const double* xsrc = (it == 1) ? a.x0 : a.x;
-  const double* pin = (it & 1) ? a.pbuf[0] : a.pbuf[1];
+  const double* xsrc = a.phase == 0 ? a.x0 : a.x;
+  const double* pin = pcg_pnew(a);
   double acc[3][V] = {};
   const long total = static_cast<long>(topo.n) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  bool checked = false;
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
@@ -204,6 +270,10 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
     const Row<V> p = ldg_row<V>(pin + o);
     const Row<V> q = ldg_row<V>(a.q + o);
     const double id = topo.inv_diag(v);
+    if (!checked) {
+      if (!active) return;  // solve already finished (uniform across the grid)
+      checked = true;
+    }
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       if (act[k]) {
@@ -218,38 +288,11 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
     st_row<V>(a.x + o, x);
     st_row<V>(a.r + o, r);
   }
+  if (!active) return;
   block_reduce_store<3, D, V>(acc, a.partials);
   __shared__ double tot[3][D];
   if (!grid_reduce_last<3, D>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x == 0) {
-    Ctl* cw = a.ctl;
-    int any = 0;
-    for (int j = 0; j < D; ++j) {
-      PcgCol& col = cw->col[j];
-      if (col.status != kActive) continue;
-      if (tot[2][j] > 0.0) {  // pcg.cpp:75
-        col.status = kFailed;
-        col.iters = 0;
-        col.rel = __longlong_as_double(0x7ff0000000000000ll);
-        cw->need_fix = 1;
-        continue;
-      }
-      col.rel = sqrt(tot[0][j]) / col.bnorm;
-      col.iters = it;
-      if (col.rel <= a.tol) {
-        col.status = kConverged;
-      } else if (it >= a.max_iter) {
-        col.status = kMaxIter;
-      } else {
-        col.beta = tot[1][j] / col.rz;
-        col.rz = tot[1][j];
-        any = 1;
-      }
-    }
-    cw->iter = it;
-    cw->any_active = any;
-    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
-  }
+  if (threadIdx.x < 32) pcg_update_epilogue<D>(a, tot, a.ctl->iter + 1);
 }
 
 // --------------------------------------------------------- PCG finalize -----
@@ -258,15 +301,17 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
 // appends the per-column report of this solve to the PCG log.
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_pcg_finalize(int n, const double* __restrict__ x0, double* x, Ctl* ctl) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int j = threadIdx.x;
     const int idx = ctl->inner_count;
-    if (idx < ctl->log_cap) {
-      for (int j = 0; j < D; ++j) {
-        ctl->log_iters[static_cast<long>(idx) * D + j] = ctl->col[j].iters;
-        ctl->log_status[static_cast<long>(idx) * D + j] = ctl->col[j].status;
-        ctl->log_rel[static_cast<long>(idx) * D + j] = ctl->col[j].rel;
-      }
+    if (j < D && idx < ctl->log_cap) {
+      const PcgCol col = ctl->col[j];
+      ctl->log_iters[static_cast<long>(idx) * D + j] = col.iters;
+      ctl->log_status[static_cast<long>(idx) * D + j] = col.status;
+      ctl->log_rel[static_cast<long>(idx) * D + j] = col.rel;
     }
+    __syncwarp();
+    if (j == 0) ctl->inner_count = idx + 1;  // no other block reads inner_count
   }
   if (!ctl->need_fix) return;
   const bool never_iterated = ctl->iter == 0;

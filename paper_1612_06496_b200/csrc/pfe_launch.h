@@ -24,8 +24,9 @@ struct TopoDesc {
 };
 
 struct Launch {
-  int grid;             // blocks
+  int grid;             // blocks (vertex-parallel kernels)
   cudaStream_t stream;
+  int sm = 148;         // multiprocessors (tiled kernels size their own grid)
 };
 
 struct LaunchTable {

@@ -1,13 +1,25 @@
 // Template bodies of the launch table (included by pfe_kernels_d*.cu only).
 #pragma once
 
+#include <stdexcept>
+#include <string>
+
 #include "pfe_kernels.cuh"
 #include "pfe_launch.h"
 #include "pfe_polar.cuh"
+#include "pfe_stencil.cuh"
 
 namespace pfe_host {
 
 using namespace pfe_dev;
+
+// Every launch is checked: a failed launch (bad configuration, resources)
+// must surface as an error, never as silently missing work.
+inline void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
+}
+#define PFE_LAUNCHED(name) check_launch(name)
 
 template <int D>
 struct Impl {
@@ -26,68 +38,100 @@ struct Impl {
     }
   }
 
+  // Tiled stencil kernels: grid = min(tiles, resident blocks), dynamic smem.
+  template <int R, auto Kern>
+  static int tiled_grid(size_t smem, const Grid<R>& g, int sm) {
+    using G = TileGeo<R, D>;
+    static int per_sm = -1;  // one value per kernel instantiation
+    if (per_sm < 0) {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int nb = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, Kern, G::NT, smem);
+      per_sm = nb < 1 ? 1 : nb;
+    }
+    const long tiles = static_cast<long>((g.W + G::TW - 1) / G::TW) * ((g.H + G::TH - 1) / G::TH);
+    return static_cast<int>(tiles < static_cast<long>(per_sm) * sm ? tiles : static_cast<long>(per_sm) * sm);
+  }
+  template <int R>
+  static void grid_init(const Grid<R>& g, const PcgArgs& a, Launch l) {
+    using G = TileGeo<R, D>;
+    constexpr size_t sm_bytes = sizeof(double) * G::kInit;
+    const int grid = tiled_grid<R, k_grid_pcg_init<D, R>>(sm_bytes, g, l.sm);
+    k_grid_pcg_init<D, R><<<grid, G::NT, sm_bytes, l.stream>>>(g, a); PFE_LAUNCHED(__func__);
+  }
+  template <int R>
+  static void grid_spmv(const Grid<R>& g, const PcgArgs& a, Launch l) {
+    using G = TileGeo<R, D>;
+    constexpr size_t sm_bytes = sizeof(double) * G::kSpmv;
+    const int grid = tiled_grid<R, k_grid_pcg_spmv<D, R>>(sm_bytes, g, l.sm);
+    k_grid_pcg_spmv<D, R><<<grid, G::NT, sm_bytes, l.stream>>>(g, a); PFE_LAUNCHED(__func__);
+  }
+  template <int R>
+  static void grid_sb(const Grid<R>& g, const SbArgs& a, Launch l) {
+    using G = TileGeo<R, D>;
+    constexpr size_t sm_bytes = sizeof(double) * G::kSb;
+    const int grid = tiled_grid<R, k_grid_sb_pass<D, R>>(sm_bytes, g, l.sm);
+    k_grid_sb_pass<D, R><<<grid, G::NT, sm_bytes, l.stream>>>(g, a); PFE_LAUNCHED(__func__);
+  }
+
   static void pcg_init(const TopoDesc& t, const PcgArgs& a, Launch l) {
-    on_topo(t, [&](const auto& topo) {
-      using T = std::decay_t<decltype(topo)>;
-      k_pcg_init<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, a);
-    });
+    if (t.kind == kTopoGrid1) return grid_init<1>(t.g1, a, l);
+    if (t.kind == kTopoGrid2) return grid_init<2>(t.g2, a, l);
+    k_pcg_init<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void pcg_spmv(const TopoDesc& t, const PcgArgs& a, Launch l) {
-    on_topo(t, [&](const auto& topo) {
-      using T = std::decay_t<decltype(topo)>;
-      k_pcg_spmv<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, a);
-    });
+    if (t.kind == kTopoGrid1) return grid_spmv<1>(t.g1, a, l);
+    if (t.kind == kTopoGrid2) return grid_spmv<2>(t.g2, a, l);
+    k_pcg_spmv<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void pcg_update(const TopoDesc& t, const PcgArgs& a, Launch l) {
     on_topo(t, [&](const auto& topo) {
       using T = std::decay_t<decltype(topo)>;
-      k_pcg_update<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, a);
+      k_pcg_update<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, a); PFE_LAUNCHED(__func__);
     });
   }
   static void pcg_finalize(int n, const double* x0, double* x, Ctl* ctl, Launch l) {
-    k_pcg_finalize<D><<<l.grid, kBlock, 0, l.stream>>>(n, x0, x, ctl);
-    k_inner_done<<<1, 32, 0, l.stream>>>(ctl);
+    k_pcg_finalize<D><<<l.grid, kBlock, 0, l.stream>>>(n, x0, x, ctl); PFE_LAUNCHED(__func__);
   }
   static void sb_pass(const TopoDesc& t, const SbArgs& a, Launch l) {
-    on_topo(t, [&](const auto& topo) {
-      using T = std::decay_t<decltype(topo)>;
-      k_sb_pass<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, a);
-    });
+    if (t.kind == kTopoGrid1) return grid_sb<1>(t.g1, a, l);
+    if (t.kind == kTopoGrid2) return grid_sb<2>(t.g2, a, l);
+    k_sb_pass<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void rhs_from_state(const TopoDesc& t, const double* s, const double* b, const double* rq, double* rhs,
                              double hl, Launch l) {
     on_topo(t, [&](const auto& topo) {
       using T = std::decay_t<decltype(topo)>;
-      k_rhs_from_state<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, s, b, rq, rhs, hl);
+      k_rhs_from_state<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, s, b, rq, rhs, hl); PFE_LAUNCHED(__func__);
     });
   }
   static void rhs_quad(int n, const double* sqd, const double* p, const double* b, double* rq, double hr, Launch l) {
-    k_rhs_quad<D><<<l.grid, kBlock, 0, l.stream>>>(n, sqd, p, b, rq, hr);
+    k_rhs_quad<D><<<l.grid, kBlock, 0, l.stream>>>(n, sqd, p, b, rq, hr); PFE_LAUNCHED(__func__);
   }
   static void objective(const TopoDesc& t, const double* y, double* partials, Ctl* ctl, Launch l) {
     on_topo(t, [&](const auto& topo) {
       using T = std::decay_t<decltype(topo)>;
-      k_objective<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, y, partials, ctl);
+      k_objective<D, T><<<l.grid, kBlock, 0, l.stream>>>(topo, y, partials, ctl); PFE_LAUNCHED(__func__);
     });
   }
   static void diff_norms(int n, const double* ynew, const double* yold, double* partials, Ctl* ctl, Launch l) {
-    k_diff_norms<D><<<l.grid, kBlock, 0, l.stream>>>(n, ynew, yold, partials, ctl);
+    k_diff_norms<D><<<l.grid, kBlock, 0, l.stream>>>(n, ynew, yold, partials, ctl); PFE_LAUNCHED(__func__);
   }
   static void tsqr_local(int n, const double* y, const double* sqd, const double* breg, double* rbuf, Launch l) {
-    k_tsqr_local<D><<<l.grid, kBlock, 0, l.stream>>>(n, y, sqd, breg, rbuf);
+    k_tsqr_local<D><<<l.grid, kBlock, 0, l.stream>>>(n, y, sqd, breg, rbuf); PFE_LAUNCHED(__func__);
   }
   static void tsqr_final(int nblk, const double* rbuf, double* w, Ctl* ctl, Launch l) {
-    k_tsqr_final<D><<<1, kBlock, 0, l.stream>>>(nblk, rbuf, w, ctl);
+    k_tsqr_final<D><<<1, kBlock, 0, l.stream>>>(nblk, rbuf, w, ctl); PFE_LAUNCHED(__func__);
   }
   static void project_apply(int n, const double* y, const double* sqd, double* breg, const double* w, double* p,
                             double* rq, double hr, Launch l) {
-    k_project_apply<D><<<l.grid, kBlock, 0, l.stream>>>(n, y, sqd, breg, w, p, rq, hr);
+    k_project_apply<D><<<l.grid, kBlock, 0, l.stream>>>(n, y, sqd, breg, w, p, rq, hr); PFE_LAUNCHED(__func__);
   }
   static int max_blocks_per_sm() {
     int worst = 8, nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_spmv<D, Grid<2>>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_spmv<D, Csr>, kBlock, 0);
     worst = nb < worst ? nb : worst;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sb_pass<D, Grid<2>>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sb_pass<D, Csr>, kBlock, 0);
     worst = nb < worst ? nb : worst;
     return worst < 1 ? 1 : worst;
   }

@@ -225,9 +225,9 @@ struct pfe_solver {
     return static_cast<int>(std::max<long>(1, std::min<long>((threads + pfe_dev::kBlock - 1) / pfe_dev::kBlock, max_grid)));
   }
   int tpv() const { return (d == 2 || d == 4 || d == 8 || d == 16) ? d / 2 : 1; }
-  pfe_host::Launch lv() const { return {grid_for(static_cast<long>(n) * tpv()), stream}; }      // vertex kernels
-  pfe_host::Launch le() const { return {grid_for(static_cast<long>(n) * d), stream}; }         // elementwise
-  pfe_host::Launch lr() const { return {grid_for(n), stream}; }                                // row kernels
+  pfe_host::Launch lv() const { return {grid_for(static_cast<long>(n) * tpv()), stream, sm}; }  // vertex kernels
+  pfe_host::Launch le() const { return {grid_for(static_cast<long>(n) * d), stream, sm}; }     // elementwise
+  pfe_host::Launch lr() const { return {grid_for(n), stream, sm}; }                            // row kernels
 
   void ensure_log(long extra) {
     const long need = inner_launched + extra;
@@ -625,6 +625,7 @@ PcgArgs pcg_args(pfe_state* st, const double* rhs) {
   a.tol = S->prm.pcg_rel_tol;
   a.max_iter = S->prm.pcg_max_iter;
   a.use_cond = 0;
+  a.phase = 0;
   return a;
 }
 
@@ -652,6 +653,7 @@ void pcg_solve_host(pfe_state* st, const double* rhs) {
   while (launched < maxit) {
     const int chunk = launched == 0 ? std::max(1, std::min(S->pred_iters, maxit)) : 1;
     for (int c = 0; c < chunk && launched < maxit; ++c, ++launched) {
+      a.phase = pfe_dev::pcg_phase(launched + 1);
       S->prof.begin(1, S->stream);
       S->tab->pcg_spmv(S->topo, a, L);
       S->prof.end(S->stream);
@@ -683,11 +685,18 @@ void pcg_solve_captured(pfe_state* st, const double* rhs) {
   const cudaGraphNode_t* deps = nullptr;
   size_t nd = 0;
   CK(cudaStreamGetCaptureInfo(S->stream, &cs, nullptr, &g, &deps, &nd));
+  if (cs != cudaStreamCaptureStatusActive || g == nullptr)
+    throw Error(PFE_CUDA_ERROR, "graph capture was invalidated before the PCG loop");
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
   a.cond = h;
   a.use_cond = 1;
   S->tab->pcg_init(S->topo, a, L);
+  // iteration 1 peeled (p comes from init, x from x0); the WHILE body then
+  // runs iterations 2k and 2k+1 with static buffer parities.
+  a.phase = 0;
+  S->tab->pcg_spmv(S->topo, a, L);
+  S->tab->pcg_update(S->topo, a, L);
   CK(cudaGetLastError());
   CK(cudaStreamGetCaptureInfo(S->stream, &cs, nullptr, &g, &deps, &nd));
   cudaGraphNodeParams np{};
@@ -700,8 +709,11 @@ void pcg_solve_captured(pfe_state* st, const double* rhs) {
   CK(cudaStreamUpdateCaptureDependencies(S->stream, &node, 1, cudaStreamSetCaptureDependencies));
   cudaGraph_t body = np.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(S->aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  S->tab->pcg_spmv(S->topo, a, {L.grid, S->aux});
-  S->tab->pcg_update(S->topo, a, {L.grid, S->aux});
+  for (int ph : {2, 1}) {
+    a.phase = ph;
+    S->tab->pcg_spmv(S->topo, a, {L.grid, S->aux, S->sm});
+    S->tab->pcg_update(S->topo, a, {L.grid, S->aux, S->sm});
+  }
   CK(cudaGetLastError());
   CK(cudaStreamEndCapture(S->aux, &body));
   S->tab->pcg_finalize(S->n, st->y, st->y2, S->ctl, S->le());
@@ -876,7 +888,7 @@ void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, v
     const Book pre{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
     const long inner0 = S->inner_launched;
     cudaGraph_t graph;
-    CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal));
+    CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeRelaxed));
     try {
       body(RunMode{true, nullptr, nullptr});
     } catch (...) {
