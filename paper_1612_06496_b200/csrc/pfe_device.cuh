@@ -39,7 +39,8 @@ struct PcgCol {
 
 // Device-resident control block shared by the kernels of one solver.
 struct Ctl {
-  PcgCol col[kMaxD];
+  PcgCol col[kMaxD];   // per-column state after the latest SpMV prologue
+  PcgCol colu[kMaxD];  // per-column state after the latest update prologue
   int iter;          // PCG iterations executed in the current solve
   int any_active;    // PCG loop condition
   int need_fix;      // finalize must patch some column of the result

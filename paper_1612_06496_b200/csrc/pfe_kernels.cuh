@@ -1,18 +1,28 @@
 // Hot-path kernels of the PFE nested Bregman loop (templates; instantiated per
 // topology and embedding dimension in pfe_kernels_*.cu).
 //
-//   k_pcg_init    r = b - A x0, p = D^-1 r, ||b||^2, r.r, r.z      (pcg.cpp:49-66)
-//   k_pcg_spmv    p = D^-1 r + beta p (fused), q = A p, p.q, alpha (pcg.cpp:68-72, 86-88)
-//   k_pcg_update  x += alpha p, r -= alpha q, r.r, r.D^-1 r, beta  (pcg.cpp:73-85)
-//   k_pcg_finalize  per-column result selection + PCG log          (pcg.cpp:50-53, 56-62, 101-112)
-//   k_sb_pass     M Y, shrink, Bregman b update, next rhs           (solver.cpp:83-84, 96-98)
-//   k_rhs_quad / k_rhs_from_state                                   (solver.cpp:79-84)
-//   k_objective   sum |M Y|                                         (solver.cpp:14-17)
+//   k_pcg_init    r = b - A x0, p = D^-1 r, partials of ||b||^2, r.r, r.z  (pcg.cpp:49-66)
+//   k_pcg_spmv    [stop test, beta] p = D^-1 r + beta p, q = A p, partial p.q
+//                                                              (pcg.cpp:56-62, 68-72, 79-88)
+//   k_pcg_update  [alpha] x += alpha p, r -= alpha q, partials r.r, r.D^-1 r, NaN
+//                                                              (pcg.cpp:71-78)
+//   k_pcg_finalize  per-column result selection + PCG log      (pcg.cpp:50-53, 56-62, 101-112)
+//   k_sb_pass     M Y, shrink, Bregman b update, next rhs       (solver.cpp:83-84, 96-98)
+//   k_rhs_quad / k_rhs_from_state                               (solver.cpp:79-84)
+//   k_objective   sum |M Y|                                     (solver.cpp:14-17)
+//
 // All d columns are iterated together; each column keeps its own alpha,
 // beta, residual and stopping state exactly as solve_multi runs them one by
-// one (pcg.cpp:94-114).  Kernels read the PCG iteration index from the
-// device control block, so the same launch sequence works inside a CUDA
-// graph whose PCG loop is a conditional WHILE node.
+// one (pcg.cpp:94-114).
+//
+// Reductions are consumer-side: a kernel only writes its per-block partial
+// sums; every block of the NEXT kernel reduces them (same fixed order in
+// every block, so all blocks derive bit-identical scalars) while its own data
+// loads are in flight, runs the scalar logic of pcg.cpp (alpha, beta,
+// convergence, breakdown) in warp 0, and block 0 persists the per-column
+// state to the control block.  No kernel has a serial last-block tail.  The
+// stop decision for iteration k is taken by the SpMV of iteration k+1, which
+// then exits immediately and clears the CUDA-graph loop condition.
 #pragma once
 
 #include "pfe_device.cuh"
@@ -27,7 +37,11 @@ struct PcgArgs {
   double* pbuf[2];     // ping-pong search directions
   double* q;
   Ctl* ctl;
-  double* partials;
+  double* part_a;      // partials of init / update (3 x D pairs, pair-major)
+  double* part_b;      // partials of spmv (D pairs)
+  int nb_init;         // block counts of the producers (consumers reduce that many)
+  int nb_update;
+  int nb_spmv;
   double tol;
   int max_iter;
   cudaGraphConditionalHandle cond;  // loop handle when running inside a graph
@@ -43,102 +57,163 @@ __host__ __device__ __forceinline__ int pcg_phase(int it) { return it == 1 ? 0 :
 __device__ __forceinline__ double* pcg_pnew(const PcgArgs& a) { return a.phase == 2 ? a.pbuf[1] : a.pbuf[0]; }
 __device__ __forceinline__ const double* pcg_pold(const PcgArgs& a) { return a.phase == 1 ? a.pbuf[1] : a.pbuf[0]; }
 
-// Scalar epilogues, run by warp 0 of the last block (see grid_reduce_last):
-// lane j owns column j, loads its PcgCol once, updates it in registers and
-// writes it back, so the epilogue costs one control-block round trip instead
-// of a dependent chain per field.
 constexpr double kInf = __builtin_huge_val();
 
-template <int D, int NQ>
-__device__ __forceinline__ void pcg_init_epilogue(const PcgArgs& a, const double (&tot)[NQ][D]) {
-  const int j = threadIdx.x;
-  bool act = false, fix = false;
-  if (j < D) {
-    PcgCol col{};
-    col.bnorm = sqrt(tot[0][j]);
-    if (col.bnorm == 0.0) {
-      col.status = kZeroRhs;
-      col.rel = 0.0;
-    } else {
-      col.rel = sqrt(tot[1][j]) / col.bnorm;
-      if (col.rel <= a.tol) {
-        col.status = kConvInit;
-      } else {
-        col.status = kActive;
-        col.rz = tot[2][j];
-      }
+// Block-wide fixed-order reduction of a producer's pair-major partials
+// (nb blocks x NQ*D pairs) into shared out[NQ][D]; all NT threads take part.
+template <int NQ, int D, int NT>
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nb, double (&out)[NQ][D]) {
+  constexpr int P = NQ * D;
+  constexpr int CH = P < 16 ? P : 16;
+  __shared__ double wsum[NT / 32][CH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < P; base += CH) {
+    double acc[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) acc[k] = 0.0;
+    for (int b = threadIdx.x; b < nb; b += NT) {
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (base + k < P) acc[k] += __ldcg(part + static_cast<long>(base + k) * nb + b);
     }
-    act = col.status == kActive;
-    fix = !act;
-    a.ctl->col[j] = col;
-  }
-  const bool any = __any_sync(0xffffffffu, act), anyfix = __any_sync(0xffffffffu, fix);
-  if (j == 0) {
-    a.ctl->iter = 0;
-    a.ctl->any_active = any;
-    a.ctl->need_fix = anyfix;
-    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < CH; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < CH; ++k) wsum[warp][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < CH && base + threadIdx.x < P) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) s += wsum[w][threadIdx.x];
+      const int pr = base + threadIdx.x;
+      out[pr / D][pr % D] = s;
+    }
+    __syncthreads();
   }
 }
 
-template <int D, int NQ>
-__device__ __forceinline__ void pcg_spmv_epilogue(const PcgArgs& a, const double (&tot)[NQ][D]) {
-  const int j = threadIdx.x;
-  bool failed = false;
-  if (j < D) {
-    PcgCol col = a.ctl->col[j];
-    if (col.status == kActive) {
-      const double pq = tot[0][j];
-      col.pq = pq;
-      if (!(pq > 0.0) || !isfinite(pq)) {  // pcg.cpp:71-72
-        col.status = kFailed;
-        col.iters = 0;
-        col.rel = kInf;
-        failed = true;
-      } else {
-        col.alpha = col.rz / pq;
-      }
-      a.ctl->col[j] = col;
-    }
-  }
-  if (__any_sync(0xffffffffu, failed) && j == 0) a.ctl->need_fix = 1;
-}
+// Column state is double-buffered in the control block: SpMV prologues read
+// Ctl::colu (written by the previous update) and write Ctl::col; update
+// prologues read Ctl::col and write Ctl::colu.
 
-template <int D, int NQ>
-__device__ __forceinline__ void pcg_update_epilogue(const PcgArgs& a, const double (&tot)[NQ][D], int it) {
-  const int j = threadIdx.x;
-  bool act = false, failed = false;
-  if (j < D) {
-    PcgCol col = a.ctl->col[j];
-    if (col.status == kActive) {
-      if (tot[2][j] > 0.0) {  // pcg.cpp:75
-        col.status = kFailed;
-        col.iters = 0;
-        col.rel = kInf;
-        failed = true;
-      } else {
-        col.rel = sqrt(tot[0][j]) / col.bnorm;
-        col.iters = it;
-        if (col.rel <= a.tol) {
-          col.status = kConverged;
-        } else if (it >= a.max_iter) {
-          col.status = kMaxIter;
+// Shared per-block view of the column state after a prologue.
+template <int D>
+struct ColView {
+  double coef[D];  // beta (spmv) or alpha (update); 0 for inactive columns
+  int act[D];
+  int any;
+};
+
+// SpMV prologue: the stop test of the previous iteration (or the initial
+// residual test after init) and beta.  Mirrors pcg.cpp:50-62 (init) and
+// pcg.cpp:75-88 (after an update).  Returns whether any column is active.
+template <int D, int NT>
+__device__ __forceinline__ bool spmv_prologue(const PcgArgs& a, ColView<D>& cv) {
+  __shared__ double tot[3][D];
+  const bool first = a.phase == 0;
+  reduce_partials<3, D, NT>(a.part_a, first ? a.nb_init : a.nb_update, tot);
+  if (threadIdx.x < 32) {
+    const int j = threadIdx.x;
+    const int done = a.ctl->iter;  // PCG iterations completed so far
+    bool act = false;
+    if (j < D) {
+      PcgCol col;
+      if (first) {  // tot = ||b||^2, r.r, r.z of the initial residual
+        col = PcgCol{};
+        col.bnorm = sqrt(tot[0][j]);
+        if (col.bnorm == 0.0) {
+          col.status = kZeroRhs;
+          col.rel = 0.0;
         } else {
-          col.beta = tot[1][j] / col.rz;
-          col.rz = tot[1][j];
-          act = true;
+          col.rel = sqrt(tot[1][j]) / col.bnorm;
+          if (col.rel <= a.tol) {
+            col.status = kConvInit;
+          } else {
+            col.status = kActive;
+            col.rz = tot[2][j];
+          }
+        }
+      } else {  // tot = r.r, r.D^-1 r, NaN count of iteration `done`
+        col = a.ctl->colu[j];
+        if (col.status == kActive) {
+          if (tot[2][j] > 0.0) {  // pcg.cpp:75
+            col.status = kFailed;
+            col.iters = 0;
+            col.rel = kInf;
+          } else {
+            col.rel = sqrt(tot[0][j]) / col.bnorm;
+            col.iters = done;
+            if (col.rel <= a.tol) {
+              col.status = kConverged;
+            } else if (done >= a.max_iter) {
+              col.status = kMaxIter;
+            } else {
+              col.beta = tot[1][j] / col.rz;
+              col.rz = tot[1][j];
+            }
+          }
         }
       }
-      a.ctl->col[j] = col;
+      act = col.status == kActive;
+      cv.act[j] = act;
+      cv.coef[j] = act ? col.beta : 0.0;
+      if (blockIdx.x == 0) a.ctl->col[j] = col;
+    }
+    const bool any = __any_sync(0xffffffffu, act);
+    if (j == 0) {
+      cv.any = any;
+      if (blockIdx.x == 0) {
+        a.ctl->any_active = any;
+        if (first) a.ctl->iter = 0;
+        if (!any && a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+      }
     }
   }
-  const bool any = __any_sync(0xffffffffu, act), anyfail = __any_sync(0xffffffffu, failed);
-  if (j == 0) {
-    a.ctl->iter = it;
-    a.ctl->any_active = any;
-    if (anyfail) a.ctl->need_fix = 1;
-    if (a.use_cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
+  __syncthreads();
+  return cv.any != 0;
+}
+
+// Update prologue: alpha = rz / p.q with the curvature check (pcg.cpp:70-72).
+template <int D, int NT>
+__device__ __forceinline__ bool update_prologue(const PcgArgs& a, ColView<D>& cv) {
+  __shared__ double tot[1][D];
+  const int active = a.ctl->any_active;  // written by this iteration's SpMV
+  if (!active) return false;             // uniform across the grid
+  reduce_partials<1, D, NT>(a.part_b, a.nb_spmv, tot);
+  if (threadIdx.x < 32) {
+    const int j = threadIdx.x;
+    bool act = false;
+    if (j < D) {
+      PcgCol col = a.ctl->col[j];
+      if (col.status == kActive) {
+        const double pq = tot[0][j];
+        col.pq = pq;
+        if (!(pq > 0.0) || !isfinite(pq)) {
+          col.status = kFailed;
+          col.iters = 0;
+          col.rel = kInf;
+        } else {
+          col.alpha = col.rz / pq;
+        }
+      }
+      // the state is double-buffered (col -> colu) so no block reads a
+      // column another block of the same kernel has already advanced
+      if (blockIdx.x == 0) a.ctl->colu[j] = col;
+      act = col.status == kActive;
+      cv.act[j] = act;
+      cv.coef[j] = act ? col.alpha : 0.0;
+    }
+    const bool any = __any_sync(0xffffffffu, act);
+    if (j == 0) {
+      cv.any = any;
+      if (blockIdx.x == 0) a.ctl->iter = a.ctl->iter + 1;
+    }
   }
+  __syncthreads();
+  return true;  // even with every column failed, write (inert) partials
 }
 
 // ---------------------------------------------------------------- PCG init --
@@ -171,23 +246,20 @@ __global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
     st_row<V>(a.r + static_cast<long>(v) * D + c0, r);
     st_row<V>(a.pbuf[0] + static_cast<long>(v) * D + c0, z);
   }
-  block_reduce_store<3, D, V>(acc, a.partials);
-  __shared__ double tot[3][D];
-  if (!grid_reduce_last<3, D>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x < 32) pcg_init_epilogue<D>(a, tot);
+  block_reduce_store<3, D, V>(acc, a.part_a);
 }
 
 // ------------------------------------------------------- PCG SpMV (+ p update)
 template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
-  const Ctl* c = a.ctl;
-  if (!c->any_active) return;
+  __shared__ ColView<D> cv;
+  if (!spmv_prologue<D, kBlock>(a, cv)) return;
   const bool first = a.phase == 0;
   const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
   double beta[V];
 #pragma unroll
-  for (int k = 0; k < V; ++k) beta[k] = (c->col[gfirst + k].status == kActive) ? c->col[gfirst + k].beta : 0.0;
+  for (int k = 0; k < V; ++k) beta[k] = cv.coef[gfirst + k];
   double* pnew = pcg_pnew(a);
   const double* pold = pcg_pold(a);
   double acc[1][V] = {};
@@ -233,47 +305,46 @@ __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
     }
     st_row<V>(a.q + static_cast<long>(v) * D + c0, qv);
   }
-  block_reduce_store<1, D, V>(acc, a.partials);
-  __shared__ double tot[1][D];
-  if (!grid_reduce_last<1, D>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x < 32) pcg_spmv_epilogue<D>(a, tot);
+  block_reduce_store<1, D, V>(acc, a.part_b);
 }
 
 // ----------------------------------------------------------- PCG update -----
 template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
-  const Ctl* c = a.ctl;
+  __shared__ ColView<D> cv;
   const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
-  // Control values and the first item's data are loaded together: no
-  // control-block round trip precedes the data loads.
-  const int active = c->any_active;
+  const double* xsrc = a.phase == 0 ? a.x0 : a.x;
+  const double* pin = pcg_pnew(a);
+  const long total = static_cast<long>(topo.n) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // first item's data is loaded before the prologue's reduction so both
+  // memory round trips overlap
+  Row<V> x{}, r{}, p{}, q{};
+  double id = 0.0;
+  auto load = [&](long ee) {
+    const int v = static_cast<int>(ee / TPV);
+    const long o = static_cast<long>(v) * D + static_cast<int>(ee - static_cast<long>(v) * TPV) * V;
+    x = ld_row<V>(xsrc + o);
+    r = ld_row<V>(a.r + o);
+    p = ldg_row<V>(pin + o);
+    q = ldg_row<V>(a.q + o);
+    id = topo.inv_diag(v);
+  };
+  if (e < total) load(e);
+  if (!update_prologue<D, kBlock>(a, cv)) return;
   double alpha[V];
   bool act[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) {
-    act[k] = c->col[gfirst + k].status == kActive;
-    alpha[k] = c->col[gfirst + k].alpha;
+    act[k] = cv.act[gfirst + k] != 0;
+    alpha[k] = cv.coef[gfirst + k];
   }
-  const double* xsrc = a.phase == 0 ? a.x0 : a.x;
-  const double* pin = pcg_pnew(a);
   double acc[3][V] = {};
-  const long total = static_cast<long>(topo.n) * TPV;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  bool checked = false;
-  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
-    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
-    const long o = static_cast<long>(v) * D + c0;
-    Row<V> x = ld_row<V>(xsrc + o);
-    Row<V> r = ld_row<V>(a.r + o);
-    const Row<V> p = ldg_row<V>(pin + o);
-    const Row<V> q = ldg_row<V>(a.q + o);
-    const double id = topo.inv_diag(v);
-    if (!checked) {
-      if (!active) return;  // solve already finished (uniform across the grid)
-      checked = true;
-    }
+    const long o = static_cast<long>(v) * D + static_cast<int>(e - static_cast<long>(v) * TPV) * V;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       if (act[k]) {
@@ -287,12 +358,9 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
     }
     st_row<V>(a.x + o, x);
     st_row<V>(a.r + o, r);
+    if (e + stride < total) load(e + stride);
   }
-  if (!active) return;
-  block_reduce_store<3, D, V>(acc, a.partials);
-  __shared__ double tot[3][D];
-  if (!grid_reduce_last<3, D>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x < 32) pcg_update_epilogue<D>(a, tot, a.ctl->iter + 1);
+  block_reduce_store<3, D, V>(acc, a.part_a);
 }
 
 // --------------------------------------------------------- PCG finalize -----
@@ -301,26 +369,33 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
 // appends the per-column report of this solve to the PCG log.
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_pcg_finalize(int n, const double* __restrict__ x0, double* x, Ctl* ctl) {
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
+  __shared__ int mode[D];  // 0 keep, 1 from x0, 2 zero
+  __shared__ int need;
+  if (threadIdx.x < 32) {
     const int j = threadIdx.x;
-    const int idx = ctl->inner_count;
-    if (j < D && idx < ctl->log_cap) {
+    const bool never_iterated = ctl->iter == 0;
+    int md = 0;
+    if (j < D) {
       const PcgCol col = ctl->col[j];
-      ctl->log_iters[static_cast<long>(idx) * D + j] = col.iters;
-      ctl->log_status[static_cast<long>(idx) * D + j] = col.status;
-      ctl->log_rel[static_cast<long>(idx) * D + j] = col.rel;
+      md = col.status == kZeroRhs ? 2 : ((col.status == kConvInit || col.status == kFailed || never_iterated) ? 1 : 0);
+      mode[j] = md;
+      if (blockIdx.x == 0) {
+        const int idx = ctl->inner_count;
+        if (idx < ctl->log_cap) {
+          ctl->log_iters[static_cast<long>(idx) * D + j] = col.iters;
+          ctl->log_status[static_cast<long>(idx) * D + j] = col.status;
+          ctl->log_rel[static_cast<long>(idx) * D + j] = col.rel;
+        }
+      }
     }
-    __syncwarp();
-    if (j == 0) ctl->inner_count = idx + 1;  // no other block reads inner_count
+    const bool anyfix = __any_sync(0xffffffffu, md != 0);
+    if (j == 0) {
+      need = anyfix;
+      if (blockIdx.x == 0) ctl->inner_count = ctl->inner_count + 1;  // no other block reads it
+    }
   }
-  if (!ctl->need_fix) return;
-  const bool never_iterated = ctl->iter == 0;
-  int mode[D];  // 0 keep, 1 from x0, 2 zero
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    const int st = ctl->col[j].status;
-    mode[j] = st == kZeroRhs ? 2 : ((st == kConvInit || st == kFailed || never_iterated) ? 1 : 0);
-  }
+  __syncthreads();
+  if (!need) return;
   const long total = static_cast<long>(n) * D;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
@@ -328,12 +403,6 @@ __global__ void __launch_bounds__(kBlock) k_pcg_finalize(int n, const double* __
     if (mode[j] == 1) x[e] = x0[e];
     else if (mode[j] == 2) x[e] = 0.0;
   }
-}
-
-// Bumps the inner-iteration counter (separate tiny launch so that every
-// block of k_pcg_finalize has read the control block before it changes).
-static __global__ void k_inner_done(Ctl* ctl) {
-  if (threadIdx.x == 0) ctl->inner_count += 1;
 }
 
 // ----------------------------------------------------- split-Bregman pass ---

@@ -31,6 +31,8 @@ struct Launch {
 
 struct LaunchTable {
   int d;
+  // block counts the PCG kernels launch with (consumers reduce that many partials)
+  void (*pcg_grids)(const TopoDesc&, Launch, int* nb_init, int* nb_spmv, int* nb_update);
   void (*pcg_init)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);
   void (*pcg_spmv)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);
   void (*pcg_update)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);

@@ -74,6 +74,20 @@ struct Impl {
     k_grid_sb_pass<D, R><<<grid, G::NT, sm_bytes, l.stream>>>(g, a); PFE_LAUNCHED(__func__);
   }
 
+  static void pcg_grids(const TopoDesc& t, Launch l, int* nb_init, int* nb_spmv, int* nb_update) {
+    *nb_update = l.grid;
+    if (t.kind == kTopoGrid1) {
+      using G = TileGeo<1, D>;
+      *nb_init = tiled_grid<1, k_grid_pcg_init<D, 1>>(sizeof(double) * G::kInit, t.g1, l.sm);
+      *nb_spmv = tiled_grid<1, k_grid_pcg_spmv<D, 1>>(sizeof(double) * G::kSpmv, t.g1, l.sm);
+    } else if (t.kind == kTopoGrid2) {
+      using G = TileGeo<2, D>;
+      *nb_init = tiled_grid<2, k_grid_pcg_init<D, 2>>(sizeof(double) * G::kInit, t.g2, l.sm);
+      *nb_spmv = tiled_grid<2, k_grid_pcg_spmv<D, 2>>(sizeof(double) * G::kSpmv, t.g2, l.sm);
+    } else {
+      *nb_init = *nb_spmv = l.grid;
+    }
+  }
   static void pcg_init(const TopoDesc& t, const PcgArgs& a, Launch l) {
     if (t.kind == kTopoGrid1) return grid_init<1>(t.g1, a, l);
     if (t.kind == kTopoGrid2) return grid_init<2>(t.g2, a, l);
@@ -141,6 +155,7 @@ template <int D>
 LaunchTable make_table() {
   using I = Impl<D>;
   return LaunchTable{D,
+                     &I::pcg_grids,
                      &I::pcg_init,
                      &I::pcg_spmv,
                      &I::pcg_update,

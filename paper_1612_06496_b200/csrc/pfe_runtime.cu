@@ -195,7 +195,8 @@ struct pfe_solver {
   double *deg = nullptr, *sqd = nullptr, *diag = nullptr, *invd = nullptr;
   Ctl* ctl = nullptr;
   Ctl* h_ctl = nullptr;  // pinned mirror
-  double* partials = nullptr;
+  double* partials = nullptr;    // init / update partials (and objective, norms)
+  double* partials_b = nullptr;  // spmv partials
   int max_grid = 0;
   double* rbuf = nullptr;
   int qr_blocks = 1;
@@ -474,6 +475,7 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   S->tab = &pfe_host::table_for(d);
   S->max_grid = S->sm * S->tab->max_blocks_per_sm();
   S->partials = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * 3 * pfe_dev::kMaxD);
+  S->partials_b = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * pfe_dev::kMaxD);
   S->ctl = S->mem.alloc<Ctl>(1);
   CK(cudaMemsetAsync(S->ctl, 0, sizeof(Ctl), S->stream));
   CK(cudaMallocHost(&S->h_ctl, sizeof(Ctl)));
@@ -621,7 +623,9 @@ PcgArgs pcg_args(pfe_state* st, const double* rhs) {
   a.pbuf[1] = st->pb[1];
   a.q = st->q;
   a.ctl = S->ctl;
-  a.partials = S->partials;
+  a.part_a = S->partials;
+  a.part_b = S->partials_b;
+  S->tab->pcg_grids(S->topo, S->lv(), &a.nb_init, &a.nb_spmv, &a.nb_update);
   a.tol = S->prm.pcg_rel_tol;
   a.max_iter = S->prm.pcg_max_iter;
   a.use_cond = 0;
@@ -638,31 +642,41 @@ void warn_columns(pfe_solver* S) {
   }
 }
 
-// One PCG solve of all d columns, host-driven: iterations are launched in
-// chunks predicted from the previous solve; kernels of an already finished
-// solve exit immediately, so over-launching is harmless.
+// One PCG solve of all d columns, host-driven.  The SpMV of iteration k
+// decides whether iteration k-1 finished the solve, so the launch sequence
+// is spmv(1) [update(k) spmv(k+1)]...; the first burst is sized from the
+// previous solve's iteration count (kernels of a finished solve exit at once).
 void pcg_solve_host(pfe_state* st, const double* rhs) {
   pfe_solver* S = st->s;
   PcgArgs a = pcg_args(st, rhs);
   const auto L = S->lv();
+  const int maxit = S->prm.pcg_max_iter;
+  auto spmv = [&](int k) {
+    a.phase = pfe_dev::pcg_phase(k);
+    S->prof.begin(1, S->stream);
+    S->tab->pcg_spmv(S->topo, a, L);
+    S->prof.end(S->stream);
+  };
+  auto update = [&](int k) {
+    a.phase = pfe_dev::pcg_phase(k);
+    S->prof.begin(2, S->stream);
+    S->tab->pcg_update(S->topo, a, L);
+    S->prof.end(S->stream);
+  };
   S->prof.begin(0, S->stream);
   S->tab->pcg_init(S->topo, a, L);
   S->prof.end(S->stream);
-  int launched = 0;
-  const int maxit = S->prm.pcg_max_iter;
-  while (launched < maxit) {
-    const int chunk = launched == 0 ? std::max(1, std::min(S->pred_iters, maxit)) : 1;
-    for (int c = 0; c < chunk && launched < maxit; ++c, ++launched) {
-      a.phase = pfe_dev::pcg_phase(launched + 1);
-      S->prof.begin(1, S->stream);
-      S->tab->pcg_spmv(S->topo, a, L);
-      S->prof.end(S->stream);
-      S->prof.begin(2, S->stream);
-      S->tab->pcg_update(S->topo, a, L);
-      S->prof.end(S->stream);
+  int k = 1;
+  spmv(1);
+  for (int burst = std::max(1, S->pred_iters);; burst = 1) {
+    for (int b = 1; b < burst && k <= maxit; ++b) {
+      update(k);
+      spmv(++k);
     }
     S->read_ctl();
-    if (!S->h_ctl->any_active) break;
+    if (!S->h_ctl->any_active || k > maxit) break;
+    update(k);
+    spmv(++k);
   }
   S->pred_iters = std::max(1, S->h_ctl->iter);
   warn_columns(S);
@@ -687,8 +701,8 @@ void pcg_solve_captured(pfe_state* st, const double* rhs) {
   CK(cudaStreamGetCaptureInfo(S->stream, &cs, nullptr, &g, &deps, &nd));
   if (cs != cudaStreamCaptureStatusActive || g == nullptr)
     throw Error(PFE_CUDA_ERROR, "graph capture was invalidated before the PCG loop");
-  cudaGraphConditionalHandle h;
-  CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  cudaGraphConditionalHandle h;  // 1 at every graph launch; the deciding SpMV clears it
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
   a.cond = h;
   a.use_cond = 1;
   S->tab->pcg_init(S->topo, a, L);

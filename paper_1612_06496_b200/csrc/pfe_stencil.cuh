@@ -220,10 +220,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
     });
     __syncthreads();
   }
-  block_reduce_store<3, D, V, G::NT>(acc, a.partials);
-  __shared__ double tot[3][D];
-  if (!grid_reduce_last<3, D, G::NT>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x < 32) pcg_init_epilogue<D>(a, tot);
+  block_reduce_store<3, D, V, G::NT>(acc, a.part_a);  // reduced by the first SpMV
 }
 
 // ---------------------------------------------------------------- spmv ----
@@ -237,8 +234,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
   double* Iv = Rs + G::NP * D;       // inv diag halo [NP]
   double* Wt = Iv + G::NP;           // [S][NP]
   double* Dg = Wt + G::S * G::NP;    // diag interior [NV]
-  __shared__ double beta[D];
-  __shared__ int active;
+  __shared__ ColView<D> cv;
   const bool first = a.phase == 0;
   double* pnew = pcg_pnew(a);
   const double* pold = first ? a.pbuf[0] : pcg_pold(a);
@@ -254,25 +250,21 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
     }
     stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
     stage_interior<R, D, 1>(g, ti, g.diag, Dg);
-    if (!checked) {  // control block read while the copies are in flight
-      if (threadIdx.x < D) {
-        const PcgCol& col = a.ctl->col[threadIdx.x];
-        beta[threadIdx.x] = col.status == kActive ? col.beta : 0.0;
+    if (!checked) {  // stop test + beta while the copies are in flight
+      if (!spmv_prologue<D, G::NT>(a, cv)) {
+        cp_async_wait_all();
+        return;
       }
-      if (threadIdx.x == 0) active = a.ctl->any_active;
+      checked = true;
     }
     cp_async_wait_all();
     __syncthreads();
-    if (!checked) {
-      if (!active) return;
-      checked = true;
-    }
     if (!first) {
       // p_u = z_u + beta p_u, z_u = D^-1_u r_u (pcg.cpp:86-88) for every tile
       // + halo position; halo values are recomputed bit-identically.
       for (int e = threadIdx.x; e < G::NP * D; e += G::NT) {
         const int pos = e / D, c = e - pos * D;
-        P[e] = Iv[pos] * Rs[e] + beta[c] * P[e];
+        P[e] = Iv[pos] * Rs[e] + cv.coef[c] * P[e];
       }
       __syncthreads();
     }
@@ -285,15 +277,8 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
     });
     __syncthreads();
   }
-  if (!checked) {  // block without tiles still votes
-    if (threadIdx.x == 0) active = a.ctl->any_active;
-    __syncthreads();
-    if (!active) return;
-  }
-  block_reduce_store<1, D, V, G::NT>(acc, a.partials);
-  __shared__ double tot[1][D];
-  if (!grid_reduce_last<1, D, G::NT>(a.partials, a.ctl, tot)) return;
-  if (threadIdx.x < 32) pcg_spmv_epilogue<D>(a, tot);
+  if (!checked && !spmv_prologue<D, G::NT>(a, cv)) return;  // block without tiles
+  block_reduce_store<1, D, V, G::NT>(acc, a.part_b);  // reduced by the update
 }
 
 // ----------------------------------------------------- split-Bregman pass -
