@@ -250,7 +250,8 @@ def run_gpu(args, rank, world, local):
     inner_per_step = prm.soc_max * prm.sb_max_stage1
 
     # ---- device-resident timing (value)
-    solver = api.PfeSolver(g, prm, device=dev, use_graphs=not args.host_driven, warn=False)
+    solver = api.PfeSolver(g, prm, device=dev, use_graphs=not args.host_driven, warn=False,
+                           persistent=not args.no_persistent)
     st = solver.make_state(y0)
     import torch
 
@@ -278,44 +279,75 @@ def run_gpu(args, rank, world, local):
     its, _, _ = solver.pcg_log()
     last = its[-inner_per_step:]
     k_per_inner = last.max(axis=1)
-    launches_per_step = int((2 * k_per_inner + 4).sum() + 3 * prm.soc_max + 1)
+    if rep["topology"] != 0 and not args.no_persistent:
+        launches_per_step = 4 * prm.soc_max + 1  # persistent kernel + 3 projection kernels per outer, rhs_quad
+    else:
+        launches_per_step = int((2 * k_per_inner + 4).sum() + 3 * prm.soc_max + 1)
     total_inner = allreduce_sum(args.steps * inner_per_step, world)
     value = total_inner / t_max
 
-    # ---- per-kernel timing: one instrumented step (CUDA events around every launch)
-    prof = api.PfeSolver(g, prm, device=dev, use_graphs=False, warn=False, profile=True)
-    pst = prof.make_state(y0)
-    prof.run_soc(pst, prm.soc_max, prm.sb_max_stage1)
-    prof.kernel_times(reset=True)
-    flush.add_(1.0)
-    torch.cuda.synchronize()
-    pst.reset()
-    prof.run_soc(pst, prm.soc_max, prm.sb_max_stage1)
-    kt = prof.kernel_times()
-    share = {k: v[0] for k, v in kt.items()}
-    tot_ms = sum(share.values()) or 1.0
-    dom = max(("pcg_spmv", "pcg_update", "sb_pass"), key=lambda k: share[k])
+    # ---- roofline of the dominant kernel: one instrumented step after the
+    # timed region with CUDA events around every launch on the solver stream
     peak, peak_src = measured_peak()
+
+    def instrumented(persistent):
+        s = api.PfeSolver(g, prm, device=dev, use_graphs=False, warn=False, profile=True, persistent=persistent)
+        ps = s.make_state(y0)
+        s.run_soc(ps, prm.soc_max, prm.sb_max_stage1)  # warm (attributes, occupancy)
+        s.kernel_times(reset=True)
+        flush.add_(1.0)
+        torch.cuda.synchronize()
+        ps.reset()
+        before = s.report()["inner_iterations"]
+        s.run_soc(ps, prm.soc_max, prm.sb_max_stage1)
+        kt = s.kernel_times()
+        its, _, _ = s.pcg_log()
+        k_inner = its[before:].max(axis=1)
+        s.close()
+        return kt, k_inner
+
+    # multi-kernel path: per-kernel split (also the path k-NN graphs use)
+    kt_m, _ = instrumented(False)
+    share = {k: v[0] for k, v in kt_m.items()}
+    tot_ms = sum(share.values()) or 1.0
     per_kernel = {}
     for k in ("pcg_spmv", "pcg_update", "pcg_init", "sb_pass"):
-        ms, cnt = kt[k]
+        ms, cnt = kt_m[k]
         b = algorithmic_bytes(k, g.n, g.m, prm.dim)
         if cnt and b:
             gbs = b / (ms / cnt * 1e-3) / 1e9
             per_kernel[k] = {"avg_us": 1e3 * ms / cnt, "launches": cnt, "alg_bytes": b, "GB/s": gbs,
                              "frac": gbs / peak, "share": share[k] / tot_ms}
-    dk = per_kernel[dom]
-    traffic = ncu_traffic(cfg.name, dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["GB/s"], "peak": peak, "unit": "GB/s",
-                "frac": dk["GB/s"] / peak, "traffic": traffic, "peak_source": peak_src,
-                "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"],
-                "timing": "CUDA events around every launch of one instrumented (host-driven) step after the "
-                          "timed region", "kernels": per_kernel}
-    prof.close()
+    persistent_used = rep["topology"] != 0 and not args.no_persistent
+    if persistent_used:
+        # the persistent kernel runs whole split_bregman calls: its algorithmic
+        # bytes are those of every phase it executes
+        kt_p, k_inner = instrumented(True)
+        ms, cnt = kt_p["sb_persistent"]
+        bi = algorithmic_bytes("pcg_init", g.n, g.m, prm.dim)
+        bs = algorithmic_bytes("pcg_spmv", g.n, g.m, prm.dim)
+        bu = algorithmic_bytes("pcg_update", g.n, g.m, prm.dim)
+        bsb = algorithmic_bytes("sb_pass", g.n, g.m, prm.dim)
+        total_b = float(sum(bi + k * (bs + bu) + bsb for k in k_inner))
+        gbs = total_b / (ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_sb_persistent", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                    "frac": gbs / peak, "traffic": ncu_traffic(cfg.name, "k_sb_persistent"),
+                    "peak_source": peak_src, "alg_bytes_per_launch": total_b / cnt,
+                    "avg_launch_us": 1e3 * ms / cnt, "launches": cnt,
+                    "timing": "CUDA events around every launch of one instrumented step after the timed region",
+                    "kernels_multi_kernel_path": per_kernel}
+    else:
+        dom = max(("pcg_spmv", "pcg_update", "sb_pass"), key=lambda k: share[k])
+        dk = per_kernel[dom]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["GB/s"], "peak": peak, "unit": "GB/s",
+                    "frac": dk["GB/s"] / peak, "traffic": ncu_traffic(cfg.name, dom), "peak_source": peak_src,
+                    "alg_bytes_per_launch": dk["alg_bytes"], "avg_launch_us": dk["avg_us"],
+                    "timing": "CUDA events around every launch of one instrumented step after the timed region",
+                    "kernels": per_kernel}
 
     # ---- end to end through the one-call C ABI with host buffers
     gc, pc = g.to_c(), prm.to_c()
-    xc = N.pfe_exec(dev, 1, 0, 0)
+    xc = N.pfe_exec(dev, 1, 0, 0, 0 if args.no_persistent else 1)
     y0c = np.asfortranarray(y0)
     yout = np.empty(g.n * prm.dim)
     repc = N.pfe_report()
@@ -348,7 +380,9 @@ def run_gpu(args, rank, world, local):
                        "parallelism": f"{world} independent replicas" if world > 1 else "single GPU",
                        "pcg_iters_per_inner_mean": float(k_per_inner.mean()),
                        "topology": ["csr", "grid8", "grid24"][rep["topology"]],
-                       "mode": "host-driven" if args.host_driven else "cuda-graph (device WHILE loop)"},
+                       "mode": ("persistent cooperative kernel per split_bregman call"
+                                if rep["topology"] != 0 and not args.no_persistent else
+                                ("host-driven" if args.host_driven else "cuda-graph (device WHILE loop)"))},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": total_inner / e2e_max, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -369,6 +403,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--host-driven", action="store_true")
+    ap.add_argument("--no-persistent", action="store_true", help="one kernel per phase instead of the "
+                    "persistent cooperative kernel (grid graphs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
     args = ap.parse_args()

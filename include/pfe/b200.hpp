@@ -151,6 +151,7 @@ struct ExecOptions {
   bool use_graphs = true;
   bool warn = true;
   bool profile = false;
+  bool persistent = true;
 };
 
 // ----------------------------------------------------------------- graph --
@@ -257,7 +258,7 @@ inline pfe_params to_c(const PfeParams& p) {
                     p.pcg.rel_tol, p.pcg.max_iter, static_cast<int32_t>(p.pcg.preconditioner)};
 }
 inline pfe_exec to_c(const ExecOptions& x) {
-  return pfe_exec{x.device, x.use_graphs ? 1 : 0, x.warn ? 1 : 0, x.profile ? 1 : 0};
+  return pfe_exec{x.device, x.use_graphs ? 1 : 0, x.warn ? 1 : 0, x.profile ? 1 : 0, x.persistent ? 1 : 0};
 }
 
 template <class M>

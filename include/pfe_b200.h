@@ -89,6 +89,9 @@ typedef struct pfe_exec {
   int32_t warn;         /* 1: print the reference's non-converged-column
                            warning to stderr (solver.cpp:87-92) */
   int32_t profile;      /* 1: time every kernel launch with CUDA events */
+  int32_t persistent;   /* 1: pixel-grid graphs run each split_bregman call as
+                           one persistent cooperative kernel (grid barriers,
+                           device-side PCG control); 0: one kernel per phase */
 } pfe_exec;
 
 /* Run report (PcgReport aggregation, pcg.hpp:21-26). */
@@ -110,7 +113,8 @@ typedef struct pfe_report {
 /* Per-kernel-class timing when pfe_exec.profile = 1. */
 #define PFE_KERNEL_CLASSES 8
 /* 0 pcg_init, 1 pcg_spmv, 2 pcg_update, 3 pcg_finalize, 4 sb_pass,
- * 5 rhs (quad / from state), 6 projection (tsqr + apply), 7 other */
+ * 5 rhs (quad / from state), 6 projection (tsqr + apply),
+ * 7 persistent split-Bregman kernel */
 typedef struct pfe_kernel_times {
   double ms[PFE_KERNEL_CLASSES];
   int64_t launches[PFE_KERNEL_CLASSES];

@@ -29,7 +29,8 @@ class pfe_params(C.Structure):
 
 
 class pfe_exec(C.Structure):
-    _fields_ = [("device", C.c_int32), ("use_graphs", C.c_int32), ("warn", C.c_int32), ("profile", C.c_int32)]
+    _fields_ = [("device", C.c_int32), ("use_graphs", C.c_int32), ("warn", C.c_int32), ("profile", C.c_int32),
+                ("persistent", C.c_int32)]
 
 
 class pfe_report(C.Structure):
@@ -39,7 +40,8 @@ class pfe_report(C.Structure):
                 ("d", C.c_int32), ("pad", C.c_int32), ("setup_seconds", C.c_double)]
 
 
-KERNEL_CLASSES = ("pcg_init", "pcg_spmv", "pcg_update", "pcg_finalize", "sb_pass", "rhs", "projection", "other")
+KERNEL_CLASSES = ("pcg_init", "pcg_spmv", "pcg_update", "pcg_finalize", "sb_pass", "rhs", "projection",
+                  "sb_persistent")
 
 
 class pfe_kernel_times(C.Structure):

@@ -145,8 +145,9 @@ def degree_vector(ei, ej, w, n) -> np.ndarray:
     return d
 
 
-def _exec(device=0, use_graphs=True, warn=True, profile=False) -> N.pfe_exec:
-    return N.pfe_exec(int(device), int(bool(use_graphs)), int(bool(warn)), int(bool(profile)))
+def _exec(device=0, use_graphs=True, warn=True, profile=False, persistent=True) -> N.pfe_exec:
+    return N.pfe_exec(int(device), int(bool(use_graphs)), int(bool(warn)), int(bool(profile)),
+                      int(bool(persistent)))
 
 
 def _colmajor(a, rows=None, cols=None) -> np.ndarray:
@@ -211,13 +212,13 @@ class PfeSolver:
     """PfeSolver (solver.hpp:51-83): operator, preconditioner and topology built once on the device."""
 
     def __init__(self, graph: WeightedGraph, params: PfeParams, device: int = 0, use_graphs: bool = True,
-                 warn: bool = True, profile: bool = False):
+                 warn: bool = True, profile: bool = False, persistent: bool = True):
         lib = N.load()
         self.graph = graph
         self.params_ = params
         self._g = graph.to_c()
         self._p = params.to_c()
-        self._x = _exec(device, use_graphs, warn, profile)
+        self._x = _exec(device, use_graphs, warn, profile, persistent)
         h = C.c_void_p()
         _check(lib.pfe_solver_create(C.byref(self._g), C.byref(self._p), C.byref(self._x), C.byref(h)))
         self._h = h
@@ -300,10 +301,10 @@ class PfeSolver:
             pass
 
 
-def _solve(mode: int, g: WeightedGraph, params: PfeParams, y0, device=0, use_graphs=True):
+def _solve(mode: int, g: WeightedGraph, params: PfeParams, y0, device=0, use_graphs=True, persistent=True):
     y0c = _colmajor(y0, g.n, params.dim)
     out = np.empty(g.n * params.dim)
-    gc, pc, xc = g.to_c(), params.to_c(), _exec(device, use_graphs)
+    gc, pc, xc = g.to_c(), params.to_c(), _exec(device, use_graphs, persistent=persistent)
     rep = N.pfe_report()
     _check(N.load().pfe_solve(C.byref(gc), C.byref(pc), C.byref(xc), mode, N.dptr(y0c), N.dptr(out),
                               C.byref(rep)))

@@ -29,6 +29,27 @@ struct Launch {
   int sm = 148;         // multiprocessors (tiled kernels size their own grid)
 };
 
+// Host view of pfe_dev::PersistArgs (topology supplied separately).
+struct PersistIn {
+  double* ybuf[2];
+  int ycur;
+  double* r;
+  double* pbuf[2];
+  double* q;
+  double* eb[2];
+  int ebcur;
+  double* es;
+  const double* rq;
+  const double* rhs0;
+  int b_zero, n_inner, write_s_last, rhs_last;
+  double tol;
+  int max_iter;
+  double hl, gamma;
+  pfe_dev::Ctl* ctl;
+  double* part;
+  double* part_b;
+};
+
 struct LaunchTable {
   int d;
   // block counts the PCG kernels launch with (consumers reduce that many partials)
@@ -49,6 +70,9 @@ struct LaunchTable {
                         double* rq, double hr, Launch);
   // Largest resident grid (blocks) of the heaviest kernels, for partial sizing.
   int (*max_blocks_per_sm)();
+  // Persistent cooperative split-Bregman kernel (grid topologies only).
+  // Returns false when the topology has no persistent kernel.
+  bool (*sb_persistent)(const TopoDesc&, const PersistIn&, Launch);
 };
 
 const LaunchTable& table_for(int d);  // d in [1, 16]

@@ -8,6 +8,7 @@
 #include "pfe_launch.h"
 #include "pfe_polar.cuh"
 #include "pfe_stencil.cuh"
+#include "pfe_persist.cuh"
 
 namespace pfe_host {
 
@@ -141,6 +142,56 @@ struct Impl {
                             double* rq, double hr, Launch l) {
     k_project_apply<D><<<l.grid, kBlock, 0, l.stream>>>(n, y, sqd, breg, w, p, rq, hr); PFE_LAUNCHED(__func__);
   }
+  template <int R>
+  static bool persist_grid(const Grid<R>& g, const PersistIn& in, Launch l) {
+    constexpr size_t smem = sizeof(double) * PersistGeo<D, R>::kSmem;
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      cudaFuncSetAttribute(k_sb_persistent<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int nb = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sb_persistent<D, R>, TileGeo<R, D>::NT, smem);
+      per_sm = nb;
+      if (per_sm < 1) throw std::runtime_error("persistent split-Bregman kernel does not fit on an SM");
+    }
+    PersistArgs<R> a{};
+    a.g = g;
+    a.ybuf[0] = in.ybuf[0];
+    a.ybuf[1] = in.ybuf[1];
+    a.ycur = in.ycur;
+    a.r = in.r;
+    a.pbuf[0] = in.pbuf[0];
+    a.pbuf[1] = in.pbuf[1];
+    a.q = in.q;
+    a.eb[0] = in.eb[0];
+    a.eb[1] = in.eb[1];
+    a.ebcur = in.ebcur;
+    a.es = in.es;
+    a.rq = in.rq;
+    a.rhs0 = in.rhs0;
+    a.b_zero = in.b_zero;
+    a.n_inner = in.n_inner;
+    a.write_s_last = in.write_s_last;
+    a.rhs_last = in.rhs_last;
+    a.tol = in.tol;
+    a.max_iter = in.max_iter;
+    a.hl = in.hl;
+    a.gamma = in.gamma;
+    a.ctl = in.ctl;
+    a.part = in.part;
+    a.part_b = in.part_b;
+    void* args[] = {&a};
+    const int grid = per_sm * l.sm;
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_sb_persistent<D, R>),
+                                                      dim3(grid), dim3(TileGeo<R, D>::NT), args, smem, l.stream);
+    if (e != cudaSuccess)
+      throw std::runtime_error(std::string("cooperative launch failed: ") + cudaGetErrorString(e));
+    return true;
+  }
+  static bool sb_persistent(const TopoDesc& t, const PersistIn& in, Launch l) {
+    if (t.kind == kTopoGrid1) return persist_grid<1>(t.g1, in, l);
+    if (t.kind == kTopoGrid2) return persist_grid<2>(t.g2, in, l);
+    return false;
+  }
   static int max_blocks_per_sm() {
     int worst = 8, nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_spmv<D, Csr>, kBlock, 0);
@@ -168,7 +219,8 @@ LaunchTable make_table() {
                      &I::tsqr_local,
                      &I::tsqr_final,
                      &I::project_apply,
-                     &I::max_blocks_per_sm};
+                     &I::max_blocks_per_sm,
+                     &I::sb_persistent};
 }
 
 }  // namespace pfe_host

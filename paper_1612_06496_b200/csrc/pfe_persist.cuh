@@ -1,0 +1,384 @@
+// Persistent cooperative split-Bregman kernel for pixel-grid graphs.
+//
+// One cooperative launch runs whole inner iterations of PfeSolver::
+// split_bregman (solver.cpp:82-107) on the device: for every inner iteration
+// the PCG solve of all d columns (init, then SpMV / update pairs until every
+// column has stopped, then the per-column result selection) followed by the
+// fused shrink / Bregman / next-rhs pass.  Phases are separated by grid-wide
+// barriers; after each barrier every block reduces the producers' block
+// partials in the same fixed order, so all blocks hold bit-identical PCG
+// scalars (alpha, beta, stop flags) in shared memory and the loop needs no
+// host round trip, no kernel launch and no serial reduction tail.
+//
+// The phases reuse the tiled, cp.async-staged stencil code of pfe_stencil.cuh
+// and produce exactly the same values as the multi-kernel path (same
+// per-element arithmetic; only the reduction tree, which depends on the grid
+// size, differs).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "pfe_stencil.cuh"
+
+namespace pfe_dev {
+
+namespace cg = cooperative_groups;
+
+template <int R>
+struct PersistArgs {
+  Grid<R> g;
+  double* ybuf[2];   // the two Y buffers
+  int ycur;          // index of Y (the warm start) at kernel start
+  double* r;         // residual; also the rhs buffer written by the sb phase
+  double* pbuf[2];
+  double* q;
+  double* eb[2];     // split_b ping-pong
+  int ebcur;
+  double* es;        // split_s (materialised on the last iteration when asked)
+  const double* rq;  // (r/2) sqrt(D) (P - B)
+  const double* rhs0;  // rhs of the first inner iteration
+  int b_zero;        // split_b == split_s == 0 at kernel start
+  int n_inner;
+  int write_s_last;
+  int rhs_last;      // produce the rhs after the last iteration too
+  double tol;
+  int max_iter;
+  double hl, gamma;
+  Ctl* ctl;
+  double* part;      // init / update block partials [3*D][gridDim.x]
+  double* part_b;    // SpMV block partials: alternating buffers so a fast block never
+                     // overwrites partials a slow block is still reducing
+};
+
+// Per-block column state (identical in every block).
+template <int D>
+struct PersistCols {
+  PcgCol col[D];
+  double coef[D];
+  int act[D];
+  int any;
+};
+
+template <int D, int R>
+struct PersistGeo {
+  using G = TileGeo<R, D>;
+  static constexpr int kSmem = G::kSpmv > G::kSb ? (G::kSpmv > G::kInit ? G::kSpmv : G::kInit)
+                                                  : (G::kSb > G::kInit ? G::kSb : G::kInit);
+};
+
+template <int D, int R>
+__global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
+  using G = TileGeo<R, D>;
+  using T = GridTopo<R>;
+  constexpr int V = G::V;
+  constexpr int NT = G::NT;
+  extern __shared__ double smem[];
+  __shared__ PersistCols<D> pc;
+  __shared__ double tot[3][D];
+  __shared__ double tot1[1][D];
+  cg::grid_group grid = cg::this_grid();
+  const Grid<R>& g = a.g;
+  const int nt = num_tiles<R, D>(g);
+  const int nb = gridDim.x;
+  int ycur = a.ycur, ebcur = a.ebcur;
+  bool b_zero = a.b_zero != 0;
+  int bad = 0;
+
+  for (int inner = 0; inner < a.n_inner; ++inner) {
+    const bool last = inner == a.n_inner - 1;
+    const double* x0 = a.ybuf[ycur];
+    double* x = a.ybuf[ycur ^ 1];
+    const double* rhs = inner == 0 ? a.rhs0 : a.r;
+
+    // ---------------- PCG init: r = b - A x0, p = D^-1 r (pcg.cpp:49-66)
+    {
+      double acc[3][V] = {};
+      double* P = smem;
+      double* Wt = P + G::NP * D;
+      double* Bv = Wt + G::S * G::NP;
+      double* Dg = Bv + G::NV * D;
+      double* Iv = Dg + G::NV;
+      for (int t = blockIdx.x; t < nt; t += nb) {
+        const TileIdx ti = tile_of<R, D>(g, t);
+        stage_rows<R, D, D>(g, ti, x0, P, G::HH);
+        stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+        stage_interior<R, D, D>(g, ti, rhs, Bv);
+        stage_interior<R, D, 1>(g, ti, g.diag, Dg);
+        stage_interior<R, D, 1>(g, ti, g.invd, Iv);
+        cp_async_wait_all();
+        __syncthreads();
+        for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
+          const double ax = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
+          const double b = Bv[tv * D + c];
+          const double rr = b - ax;
+          const double z = Iv[tv] * rr;
+          a.r[v * D + c] = rr;
+          a.pbuf[0][v * D + c] = z;
+          acc[0][k] += b * b;
+          acc[1][k] += rr * rr;
+          acc[2][k] += rr * z;
+        });
+        __syncthreads();
+      }
+      block_reduce_store<3, D, V, NT>(acc, a.part);
+    }
+    grid.sync();
+    reduce_partials<3, D, NT>(a.part, nb, tot);
+    if (threadIdx.x < 32) {  // initial residual test (pcg.cpp:50-62)
+      const int j = threadIdx.x;
+      bool act = false;
+      if (j < D) {
+        PcgCol col{};
+        col.bnorm = sqrt(tot[0][j]);
+        if (col.bnorm == 0.0) {
+          col.status = kZeroRhs;
+        } else {
+          col.rel = sqrt(tot[1][j]) / col.bnorm;
+          if (col.rel <= a.tol) {
+            col.status = kConvInit;
+          } else {
+            col.status = kActive;
+            col.rz = tot[2][j];
+          }
+        }
+        pc.col[j] = col;
+        act = col.status == kActive;
+        pc.act[j] = act;
+      }
+      const bool any = __any_sync(0xffffffffu, act);
+      if (j == 0) pc.any = any;
+    }
+    __syncthreads();
+
+    // ---------------- PCG iterations (pcg.cpp:68-89)
+    int it = 0;
+    while (pc.any && it < a.max_iter) {
+      ++it;
+      const bool first = it == 1;
+      double* pnew = (it & 1) ? a.pbuf[0] : a.pbuf[1];
+      const double* pold = first ? a.pbuf[0] : ((it & 1) ? a.pbuf[1] : a.pbuf[0]);
+      if (threadIdx.x < D) pc.coef[threadIdx.x] = pc.act[threadIdx.x] ? pc.col[threadIdx.x].beta : 0.0;
+      __syncthreads();
+      // SpMV with the fused direction update p = z + beta p
+      {
+        double acc[1][V] = {};
+        double* P = smem;
+        double* Rs = P + G::NP * D;
+        double* Iv = Rs + G::NP * D;
+        double* Wt = Iv + G::NP;
+        double* Dg = Wt + G::S * G::NP;
+        for (int t = blockIdx.x; t < nt; t += nb) {
+          const TileIdx ti = tile_of<R, D>(g, t);
+          stage_rows<R, D, D>(g, ti, pold, P, G::HH);
+          if (!first) {
+            stage_rows<R, D, D>(g, ti, a.r, Rs, G::HH);
+            stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
+          }
+          stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+          stage_interior<R, D, 1>(g, ti, g.diag, Dg);
+          cp_async_wait_all();
+          __syncthreads();
+          if (!first) {
+            for (int e = threadIdx.x; e < G::NP * D; e += NT) {
+              const int pos = e / D, c = e - pos * D;
+              P[e] = Iv[pos] * Rs[e] + pc.coef[c] * P[e];
+            }
+            __syncthreads();
+          }
+          for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
+            const double qv = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
+            const double pv = P[hpos * D + c];
+            a.q[v * D + c] = qv;
+            if (!first) pnew[v * D + c] = pv;
+            acc[0][k] += pv * qv;
+          });
+          __syncthreads();
+        }
+        block_reduce_store<1, D, V, NT>(acc, a.part_b);
+      }
+      grid.sync();
+      reduce_partials<1, D, NT>(a.part_b, nb, tot1);
+      if (threadIdx.x < 32) {  // alpha and the curvature check (pcg.cpp:70-72)
+        const int j = threadIdx.x;
+        if (j < D) {
+          PcgCol& col = pc.col[j];
+          if (pc.act[j]) {
+            const double pq = tot1[0][j];
+            col.pq = pq;
+            if (!(pq > 0.0) || !isfinite(pq)) {
+              col.status = kFailed;
+              col.iters = 0;
+              col.rel = kInf;
+              pc.act[j] = 0;
+            } else {
+              col.alpha = col.rz / pq;
+            }
+          }
+          pc.coef[j] = pc.act[j] ? col.alpha : 0.0;
+        }
+      }
+      __syncthreads();
+      // update x += alpha p, r -= alpha q (pcg.cpp:73-78); element e owns
+      // column e % D (fixed per thread when D divides the warp)
+      {
+        constexpr bool kFix = (32 % D == 0);
+        constexpr int VA = kFix ? 1 : D;
+        double acc[3][VA] = {};
+        const double* xs = first ? x0 : x;
+        const double* pin = first ? a.pbuf[0] : pnew;
+        const long total = static_cast<long>(g.n) * D;
+        const long stride = static_cast<long>(nb) * NT;
+        for (long e = static_cast<long>(blockIdx.x) * NT + threadIdx.x; e < total; e += stride) {
+          const int c = static_cast<int>(e % D);
+          const int k = kFix ? 0 : c;
+          double xv = xs[e];
+          double rv = a.r[e];
+          if (pc.act[c]) {
+            const double alpha = pc.coef[c];
+            xv = xv + alpha * __ldg(pin + e);
+            rv = rv - alpha * __ldg(a.q + e);
+            if (!isfinite(xv)) acc[2][k] += 1.0;
+          }
+          const double z = __ldg(g.invd + e / D) * rv;
+          acc[0][k] += rv * rv;
+          acc[1][k] += rv * z;
+          x[e] = xv;
+          a.r[e] = rv;
+        }
+        block_reduce_store<3, D, VA, NT>(acc, a.part);
+      }
+      grid.sync();
+      reduce_partials<3, D, NT>(a.part, nb, tot);
+      if (threadIdx.x < 32) {  // stop test and beta (pcg.cpp:75-88)
+        const int j = threadIdx.x;
+        bool act = false;
+        if (j < D) {
+          PcgCol& col = pc.col[j];
+          if (pc.act[j]) {
+            if (tot[2][j] > 0.0) {
+              col.status = kFailed;
+              col.iters = 0;
+              col.rel = kInf;
+            } else {
+              col.rel = sqrt(tot[0][j]) / col.bnorm;
+              col.iters = it;
+              if (col.rel <= a.tol) {
+                col.status = kConverged;
+              } else if (it >= a.max_iter) {
+                col.status = kMaxIter;
+              } else {
+                col.beta = tot[1][j] / col.rz;
+                col.rz = tot[1][j];
+              }
+            }
+          }
+          act = col.status == kActive;
+          pc.act[j] = act;
+        }
+        const bool any = __any_sync(0xffffffffu, act);
+        if (j == 0) pc.any = any;
+      }
+      __syncthreads();
+    }
+
+    // ---------------- result selection + log (pcg.cpp:50-62, 101-112)
+    {
+      __shared__ int mode[D];
+      if (threadIdx.x < D) {
+        const PcgCol& col = pc.col[threadIdx.x];
+        mode[threadIdx.x] =
+            col.status == kZeroRhs ? 2 : ((col.status == kConvInit || col.status == kFailed || it == 0) ? 1 : 0);
+        if (blockIdx.x == 0) {
+          a.ctl->col[threadIdx.x] = col;
+          const int idx = a.ctl->inner_count;
+          if (idx < a.ctl->log_cap) {
+            a.ctl->log_iters[static_cast<long>(idx) * D + threadIdx.x] = col.iters;
+            a.ctl->log_status[static_cast<long>(idx) * D + threadIdx.x] = col.status;
+            a.ctl->log_rel[static_cast<long>(idx) * D + threadIdx.x] = col.rel;
+          }
+        }
+      }
+      __syncthreads();
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->inner_count += 1;
+        a.ctl->iter = it;
+      }
+      bool need = false;
+#pragma unroll
+      for (int j = 0; j < D; ++j) need |= mode[j] != 0;
+      if (need) {
+        const long total = static_cast<long>(g.n) * D;
+        for (long e = static_cast<long>(blockIdx.x) * NT + threadIdx.x; e < total; e += static_cast<long>(nb) * NT) {
+          const int j = static_cast<int>(e % D);
+          if (mode[j] == 1) x[e] = x0[e];
+          else if (mode[j] == 2) x[e] = 0.0;
+        }
+      }
+    }
+    ycur ^= 1;
+    grid.sync();
+
+    // ---------------- split-Bregman pass (solver.cpp:96-98, 83-84)
+    {
+      const double* y = a.ybuf[ycur];
+      const double* b_old = b_zero ? nullptr : a.eb[ebcur];
+      double* b_new = a.eb[ebcur ^ 1];
+      double* s_out = (last && a.write_s_last) ? a.es : nullptr;
+      double* rhs_out = (!last || a.rhs_last) ? a.r : nullptr;
+      double* P = smem;
+      double* Wt = P + G::NP * D;
+      double* Rq = Wt + G::S * G::NP;
+      double* Bo = Rq + G::NV * D;
+      for (int t = blockIdx.x; t < nt; t += nb) {
+        const TileIdx ti = tile_of<R, D>(g, t);
+        stage_rows<R, D, D>(g, ti, y, P, G::HH);
+        stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+        if (rhs_out) stage_interior<R, D, D>(g, ti, a.rq, Rq);
+        if constexpr (G::kStageB) {
+          if (b_old) stage_planes<R, D, G::S, D>(g, ti, b_old, Bo, G::TH + R);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
+          bad |= !isfinite(P[hpos * D + c]);
+          double acc = 0.0;
+#pragma unroll
+          for (int e = 0; e < 2 * G::S; ++e) {
+            const bool fwd = e >= G::S;
+            const int s = fwd ? e - G::S : G::S - 1 - e;
+            const int npos = fwd ? hpos + T::dy(s) * G::HW + T::dx(s) : hpos - T::dy(s) * G::HW - T::dx(s);
+            const int opos = fwd ? hpos : npos;
+            const int jpos = fwd ? npos : hpos;
+            const double w = Wt[s * G::NP + opos];
+            if (w == 0.0) continue;
+            const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
+            double bo = 0.0;
+            if (b_old) {
+              if constexpr (G::kStageB)
+                bo = Bo[(s * G::NO + opos) * D + c];
+              else
+                bo = __ldg(b_old + slot * D + c);
+            }
+            const double nw = -w;
+            const double my = w * P[opos * D + c] + nw * P[jpos * D + c];
+            const double sh = shrink1(my + bo, a.gamma);
+            const double bn = bo + (my - sh);
+            acc += (fwd ? w : nw) * (sh - bn);
+            if (fwd) {
+              b_new[slot * D + c] = bn;
+              if (s_out) s_out[slot * D + c] = sh;
+            }
+          }
+          if (rhs_out) rhs_out[v * D + c] = a.hl * acc + Rq[tv * D + c];
+        });
+        __syncthreads();
+      }
+    }
+    ebcur ^= 1;
+    b_zero = false;
+    grid.sync();
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.ctl->nonfinite_y, 1);
+}
+
+}  // namespace pfe_dev

@@ -184,6 +184,7 @@ struct pfe_solver {
   cudaStream_t stream = nullptr, aux = nullptr;
   int sm = 148;
   bool use_graphs = true, warn = true;
+  bool persistent = true;  // grid topologies: one cooperative launch per split_bregman call
   pfe_params prm{};
   int n = 0;
   long m = 0;
@@ -468,12 +469,13 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   S->use_graphs = x ? x->use_graphs != 0 : true;
   S->warn = x ? x->warn != 0 : true;
   S->prof.on = x ? x->profile != 0 : false;
+  S->persistent = x ? x->persistent != 0 : true;
   CK(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&S->aux, cudaStreamNonBlocking));
   CK(cudaDeviceGetAttribute(&S->sm, cudaDevAttrMultiProcessorCount, S->device));
   S->d = d;
   S->tab = &pfe_host::table_for(d);
-  S->max_grid = S->sm * S->tab->max_blocks_per_sm();
+  S->max_grid = S->sm * std::max(8, S->tab->max_blocks_per_sm());
   S->partials = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * 3 * pfe_dev::kMaxD);
   S->partials_b = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * pfe_dev::kMaxD);
   S->ctl = S->mem.alloc<Ctl>(1);
@@ -766,6 +768,67 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
     S->prof.end(S->stream);
     rhs = st->r;
   }
+  auto after_iteration = [&](int it) -> bool {  // callback + relative-change test; true = stop
+    if (mode.cb) {
+      std::vector<double> yh(static_cast<size_t>(S->n) * S->d);
+      download_rows(S, st->y, S->n, S->d, yh.data(), st->q);
+      check_flags(S);
+      mode.cb(it, yh.data(), S->n, S->d, mode.user);
+    }
+    if (conv) {
+      S->tab->diff_norms(S->n, st->y, st->y2, S->partials, S->ctl, S->lr());
+      S->read_ctl();
+      const double den = std::sqrt(S->h_ctl->scalar[2]);
+      if (den > 0.0 && std::sqrt(S->h_ctl->scalar[1]) / den <= S->prm.conv_tol) return true;
+    }
+    return false;
+  };
+  if (S->persistent && !mode.captured && S->topo.kind != pfe_host::kTopoCsr) {
+    // Whole call in one cooperative launch; with a callback or the
+    // relative-change test, one launch per inner iteration.
+    const bool per_iter = mode.cb != nullptr || conv;
+    for (int it = 0; it < max_iter;) {
+      const int nrun = per_iter ? 1 : max_iter;
+      pfe_host::PersistIn in{};
+      in.ybuf[0] = st->ybuf[0];
+      in.ybuf[1] = st->ybuf[1];
+      in.ycur = st->y == st->ybuf[0] ? 0 : 1;
+      in.r = st->r;
+      in.pbuf[0] = st->pb[0];
+      in.pbuf[1] = st->pb[1];
+      in.q = st->q;
+      in.eb[0] = st->eb[0];
+      in.eb[1] = st->eb[1];
+      in.ebcur = st->eb_cur;
+      in.es = st->es;
+      in.rq = st->rq;
+      in.rhs0 = rhs;
+      in.b_zero = st->inner_zero ? 1 : 0;
+      in.n_inner = nrun;
+      in.write_s_last = 1;
+      in.rhs_last = (it + nrun < max_iter) ? 1 : 0;
+      in.tol = S->prm.pcg_rel_tol;
+      in.max_iter = S->prm.pcg_max_iter;
+      in.hl = hl;
+      in.gamma = gamma;
+      in.ctl = S->ctl;
+      in.part = S->partials;
+      in.part_b = S->partials_b;
+      S->prof.begin(7, S->stream);
+      S->tab->sb_persistent(S->topo, in, S->lv());
+      S->prof.end(S->stream);
+      for (int k = 0; k < nrun; ++k) {
+        std::swap(st->y, st->y2);
+        st->eb_cur ^= 1;
+      }
+      st->inner_zero = false;
+      S->inner_launched += nrun;
+      rhs = st->r;
+      it += nrun;
+      if (per_iter && after_iteration(it - 1)) break;
+    }
+    return;
+  }
   for (int it = 0; it < max_iter; ++it) {
     const bool last = it == max_iter - 1;
     solve_step(st, rhs, mode);
@@ -785,24 +848,7 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
     st->eb_cur ^= 1;
     st->inner_zero = false;
     rhs = st->r;
-    if (mode.cb) {
-      std::vector<double> yh(static_cast<size_t>(S->n) * S->d);
-      download_rows(S, st->y, S->n, S->d, yh.data(), st->q);
-      check_flags(S);
-      mode.cb(it, yh.data(), S->n, S->d, mode.user);
-    }
-    if (conv) {
-      S->tab->diff_norms(S->n, st->y, st->y2, S->partials, S->ctl, S->lr());
-      S->read_ctl();
-      const double den = std::sqrt(S->h_ctl->scalar[2]);
-      if (den > 0.0 && std::sqrt(S->h_ctl->scalar[1]) / den <= S->prm.conv_tol) {
-        if (!last) {
-          // the relative-change test may stop before the last iteration:
-          // rhs for a following call is rebuilt from (s, b)
-        }
-        break;
-      }
-    }
+    if (after_iteration(it)) break;
   }
 }
 
@@ -872,7 +918,9 @@ void execute(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* u
 
 void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* user) {
   pfe_solver* S = st->s;
-  const bool graphable = S->use_graphs && !cb && !(S->prm.conv_tol > 0.0) && !S->prof.on;
+  // the persistent path needs no graph (a whole call is ~3 launches per outer step)
+  const bool graphable = S->use_graphs && !cb && !(S->prm.conv_tol > 0.0) && !S->prof.on &&
+                         !(S->persistent && S->topo.kind != pfe_host::kTopoCsr);
   long planned = 0;
   if (kind == kCallSplit) planned = a0;
   if (kind == kCallSoc) planned = static_cast<long>(a0) * a1;
@@ -965,6 +1013,7 @@ pfe_exec pfe_exec_default(void) {
   x.use_graphs = 1;
   x.warn = 1;
   x.profile = 0;
+  x.persistent = 1;
   return x;
 }
 

@@ -121,7 +121,7 @@ int main() {
     pfe::Embedding a = pfe::pfe_two_stage(g, prm, y0);
     pfe::Embedding s = pfe::soc(g, prm, y0);
     CHECK(a == s);
-    pfe::PfeSolver solver(g, prm, pfe::ExecOptions{0, true, false, false});
+    pfe::PfeSolver solver(g, prm, pfe::ExecOptions{0, true, false, false, true});
     pfe::SolverState st = solver.make_state(y0);
     solver.run_soc(st, prm.soc_max, prm.sb_max_stage1);
     double dev = 0.0;

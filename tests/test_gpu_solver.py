@@ -170,9 +170,31 @@ def test_graph_and_host_driven_agree_bitwise():
     g = small_image()
     prm = jacobi(4, soc=3, sb=5)
     y0 = api.random_embedding(g.n, 4, 2, g.degree)
-    a = api.soc(g, prm, y0, use_graphs=True)
-    b = api.soc(g, prm, y0, use_graphs=False)
+    a = api.soc(g, prm, y0, use_graphs=True, persistent=False)
+    b = api.soc(g, prm, y0, use_graphs=False, persistent=False)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("radius,d", [(1, 4), (1, 8), (1, 3), (2, 8)])
+def test_persistent_kernel_matches_multi_kernel_path(radius, d):
+    """The cooperative persistent split-Bregman kernel computes the same
+    per-element arithmetic as the one-kernel-per-phase path; only the
+    reduction trees (grid sizes) differ."""
+    g = small_image(48, 70, seed=5, radius=radius, sigma_xy=2.0 if radius == 2 else None)
+    prm = jacobi(d, soc=3, sb=6)
+    y0 = api.random_embedding(g.n, d, 4, g.degree)
+    a = api.soc(g, prm, y0, persistent=True)
+    b = api.soc(g, prm, y0, persistent=False)
+    assert rel_fro_signed(a, b) <= 1e-12
+    exp = O.solve(g, prm, y0, mode=0)
+    assert rel_fro_signed(a, exp) <= 1e-10
+    # state after a persistent call is complete (split_s materialised)
+    s = api.PfeSolver(g, prm, warn=False)
+    st = s.make_state(y0)
+    s.run_soc(st, 2, 4)
+    full = O.solve(g, jacobi(d, soc=2, sb=4), y0, mode=0, full_state=True)
+    assert np.abs(st.split_s - full["split_s"]).max() <= 1e-9
+    assert np.abs(st.split_b - full["split_b"]).max() <= 1e-9
 
 
 def test_deterministic_runs():
