@@ -328,7 +328,7 @@ def run_gpu(args, rank, world, local):
         bs = algorithmic_bytes("pcg_spmv", g.n, g.m, prm.dim)
         bu = algorithmic_bytes("pcg_update", g.n, g.m, prm.dim)
         bsb = algorithmic_bytes("sb_pass", g.n, g.m, prm.dim)
-        total_b = float(sum(bi + k * (bs + bu) + bsb for k in k_inner))
+        total_b = float(sum(bi + int(k) * (bs + bu) + bsb for k in k_inner))
         gbs = total_b / (ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "kernel": "k_sb_persistent", "achieved": gbs, "peak": peak, "unit": "GB/s",
                     "frac": gbs / peak, "traffic": ncu_traffic(cfg.name, "k_sb_persistent"),

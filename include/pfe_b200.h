@@ -146,6 +146,10 @@ int pfe_solver_kernel_times(const pfe_solver* s, pfe_kernel_times* out, int rese
 /* Device time (CUDA events on the solver's stream) of the last
  * split_bregman / run_soc / two_stage call, in milliseconds. */
 double pfe_solver_last_ms(const pfe_solver* s);
+/* Phase trace of the last persistent launch (environment PFE_TRACE=1 at
+ * solver creation): entries are (phase code << 56) | %globaltimer ns,
+ * recorded by block 0 after each grid barrier.  Returns the entry count. */
+int64_t pfe_solver_trace(const pfe_solver* s, uint64_t* out, int64_t cap);
 
 /* PfeSolver::make_state (solver.cpp:60-71): Y = y0, P = sqrt(D) y0, B = 0,
  * split_b = split_s = 0.  y0 is host column-major n x dim. */

@@ -66,6 +66,7 @@ _SIGS = {
     "pfe_solver_pcg_log": (C.c_int64, [_P, _I, _I, _D, C.c_int64]),
     "pfe_solver_kernel_times": (C.c_int, [_P, C.POINTER(pfe_kernel_times), C.c_int]),
     "pfe_solver_last_ms": (C.c_double, [_P]),
+    "pfe_solver_trace": (C.c_int64, [_P, C.POINTER(C.c_uint64), C.c_int64]),
     "pfe_state_create": (C.c_int, [_P, _D, C.POINTER(_P)]),
     "pfe_state_reset": (C.c_int, [_P]),
     "pfe_state_destroy": (None, [_P]),

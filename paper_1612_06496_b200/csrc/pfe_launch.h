@@ -48,6 +48,8 @@ struct PersistIn {
   pfe_dev::Ctl* ctl;
   double* part;
   double* part_b;
+  unsigned long long* trace;  // optional phase trace (null: off)
+  int trace_cap;
 };
 
 struct LaunchTable {

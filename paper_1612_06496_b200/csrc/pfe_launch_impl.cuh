@@ -179,6 +179,8 @@ struct Impl {
     a.ctl = in.ctl;
     a.part = in.part;
     a.part_b = in.part_b;
+    a.trace = in.trace;
+    a.trace_cap = in.trace_cap;
     void* args[] = {&a};
     const int grid = per_sm * l.sm;
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_sb_persistent<D, R>),

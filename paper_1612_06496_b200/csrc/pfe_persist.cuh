@@ -10,10 +10,12 @@
 // scalars (alpha, beta, stop flags) in shared memory and the loop needs no
 // host round trip, no kernel launch and no serial reduction tail.
 //
-// The phases reuse the tiled, cp.async-staged stencil code of pfe_stencil.cuh
-// and produce exactly the same values as the multi-kernel path (same
-// per-element arithmetic; only the reduction tree, which depends on the grid
-// size, differs).
+// The stencil phases (init, SpMV) stage their tiles with double-buffered
+// cp.async: the copies of the block's next tile are in flight while the
+// current tile is evaluated from shared memory.  The update phase streams
+// with a 4-deep software pipeline (all loads of a batch issued before any
+// store).  Per-element arithmetic is exactly that of the multi-kernel path
+// (pfe_stencil.cuh / pfe_kernels.cuh); only the reduction tree differs.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -23,6 +25,17 @@
 namespace pfe_dev {
 
 namespace cg = cooperative_groups;
+
+// Optional phase trace (block 0, thread 0): code and %globaltimer after each
+// grid barrier, for the per-phase timing breakdown in scripts/prof_run.py.
+#define PFE_TRACE(code)                                                                      \
+  do {                                                                                       \
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && trace_n < a.trace_cap) {            \
+      unsigned long long t_;                                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                 \
+      a.trace[trace_n++] = (static_cast<unsigned long long>(code) << 56) | (t_ & ((1ull << 56) - 1)); \
+    }                                                                                        \
+  } while (0)
 
 template <int R>
 struct PersistArgs {
@@ -46,6 +59,8 @@ struct PersistArgs {
   double hl, gamma;
   Ctl* ctl;
   double* part;      // init / update block partials [3*D][gridDim.x]
+  unsigned long long* trace;  // optional phase trace (null: off)
+  int trace_cap;
   double* part_b;    // SpMV block partials: alternating buffers so a fast block never
                      // overwrites partials a slow block is still reducing
 };
@@ -62,9 +77,16 @@ struct PersistCols {
 template <int D, int R>
 struct PersistGeo {
   using G = TileGeo<R, D>;
-  static constexpr int kSmem = G::kSpmv > G::kSb ? (G::kSpmv > G::kInit ? G::kSpmv : G::kInit)
-                                                  : (G::kSb > G::kInit ? G::kSb : G::kInit);
+  static constexpr int kInit2 = 2 * G::kInit, kSpmv2 = 2 * G::kSpmv;
+  static constexpr int kA = kInit2 > kSpmv2 ? kInit2 : kSpmv2;
+  static constexpr int kSmem = kA > G::kSb ? kA : G::kSb;  // doubles
 };
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 template <int D, int R>
 __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
@@ -83,6 +105,8 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
   int ycur = a.ycur, ebcur = a.ebcur;
   bool b_zero = a.b_zero != 0;
   int bad = 0;
+  int trace_n = 0;
+  PFE_TRACE(0);
 
   for (int inner = 0; inner < a.n_inner; ++inner) {
     const bool last = inner == a.n_inner - 1;
@@ -93,20 +117,33 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
     // ---------------- PCG init: r = b - A x0, p = D^-1 r (pcg.cpp:49-66)
     {
       double acc[3][V] = {};
-      double* P = smem;
-      double* Wt = P + G::NP * D;
-      double* Bv = Wt + G::S * G::NP;
-      double* Dg = Bv + G::NV * D;
-      double* Iv = Dg + G::NV;
-      for (int t = blockIdx.x; t < nt; t += nb) {
+      auto stage = [&](int t, int buf) {
+        double* P = smem + buf * G::kInit;
+        double* Wt = P + G::NP * D;
+        double* Bv = Wt + G::S * G::NP;
+        double* Dg = Bv + G::NV * D;
+        double* Iv = Dg + G::NV;
         const TileIdx ti = tile_of<R, D>(g, t);
         stage_rows<R, D, D>(g, ti, x0, P, G::HH);
         stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
         stage_interior<R, D, D>(g, ti, rhs, Bv);
         stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         stage_interior<R, D, 1>(g, ti, g.invd, Iv);
-        cp_async_wait_all();
+      };
+      int buf = 0;
+      if (blockIdx.x < nt) stage(blockIdx.x, 0);
+      cp_async_commit();
+      for (int t = blockIdx.x; t < nt; t += nb) {
+        if (t + nb < nt) stage(t + nb, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
+        const double* P = smem + buf * G::kInit;
+        const double* Wt = P + G::NP * D;
+        const double* Bv = Wt + G::S * G::NP;
+        const double* Dg = Bv + G::NV * D;
+        const double* Iv = Dg + G::NV;
+        const TileIdx ti = tile_of<R, D>(g, t);
         for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
           const double ax = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
           const double b = Bv[tv * D + c];
@@ -119,10 +156,13 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
           acc[2][k] += rr * z;
         });
         __syncthreads();
+        buf ^= 1;
       }
+      cp_async_wait<0>();
       block_reduce_store<3, D, V, NT>(acc, a.part);
     }
     grid.sync();
+    PFE_TRACE(1);
     reduce_partials<3, D, NT>(a.part, nb, tot);
     if (threadIdx.x < 32) {  // initial residual test (pcg.cpp:50-62)
       const int j = threadIdx.x;
@@ -158,16 +198,15 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
       double* pnew = (it & 1) ? a.pbuf[0] : a.pbuf[1];
       const double* pold = first ? a.pbuf[0] : ((it & 1) ? a.pbuf[1] : a.pbuf[0]);
       if (threadIdx.x < D) pc.coef[threadIdx.x] = pc.act[threadIdx.x] ? pc.col[threadIdx.x].beta : 0.0;
-      __syncthreads();
       // SpMV with the fused direction update p = z + beta p
       {
         double acc[1][V] = {};
-        double* P = smem;
-        double* Rs = P + G::NP * D;
-        double* Iv = Rs + G::NP * D;
-        double* Wt = Iv + G::NP;
-        double* Dg = Wt + G::S * G::NP;
-        for (int t = blockIdx.x; t < nt; t += nb) {
+        auto stage = [&](int t, int buf) {
+          double* P = smem + buf * G::kSpmv;
+          double* Rs = P + G::NP * D;
+          double* Iv = Rs + G::NP * D;
+          double* Wt = Iv + G::NP;
+          double* Dg = Wt + G::S * G::NP;
           const TileIdx ti = tile_of<R, D>(g, t);
           stage_rows<R, D, D>(g, ti, pold, P, G::HH);
           if (!first) {
@@ -176,8 +215,20 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
           }
           stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
           stage_interior<R, D, 1>(g, ti, g.diag, Dg);
-          cp_async_wait_all();
+        };
+        int buf = 0;
+        if (blockIdx.x < nt) stage(blockIdx.x, 0);
+        cp_async_commit();
+        for (int t = blockIdx.x; t < nt; t += nb) {
+          if (t + nb < nt) stage(t + nb, buf ^ 1);
+          cp_async_commit();
+          cp_async_wait<1>();
           __syncthreads();
+          double* P = smem + buf * G::kSpmv;
+          const double* Rs = P + G::NP * D;
+          const double* Iv = Rs + G::NP * D;
+          const double* Wt = Iv + G::NP;
+          const double* Dg = Wt + G::S * G::NP;
           if (!first) {
             for (int e = threadIdx.x; e < G::NP * D; e += NT) {
               const int pos = e / D, c = e - pos * D;
@@ -185,6 +236,7 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
             }
             __syncthreads();
           }
+          const TileIdx ti = tile_of<R, D>(g, t);
           for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
             const double qv = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
             const double pv = P[hpos * D + c];
@@ -193,10 +245,13 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
             acc[0][k] += pv * qv;
           });
           __syncthreads();
+          buf ^= 1;
         }
+        cp_async_wait<0>();
         block_reduce_store<1, D, V, NT>(acc, a.part_b);
       }
       grid.sync();
+    PFE_TRACE(3);
       reduce_partials<1, D, NT>(a.part_b, nb, tot1);
       if (threadIdx.x < 32) {  // alpha and the curvature check (pcg.cpp:70-72)
         const int j = threadIdx.x;
@@ -219,35 +274,53 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
       }
       __syncthreads();
       // update x += alpha p, r -= alpha q (pcg.cpp:73-78); element e owns
-      // column e % D (fixed per thread when D divides the warp)
+      // column e % D; batches of U elements per thread are loaded before any
+      // of them is stored (the buffers alias, so the compiler cannot hoist)
       {
         constexpr bool kFix = (32 % D == 0);
         constexpr int VA = kFix ? 1 : D;
+        constexpr int U = 4;
         double acc[3][VA] = {};
-        const double* xs = first ? x0 : x;
-        const double* pin = first ? a.pbuf[0] : pnew;
+        const double* __restrict__ xs = first ? x0 : x;
+        const double* __restrict__ pin = first ? a.pbuf[0] : pnew;
         const long total = static_cast<long>(g.n) * D;
         const long stride = static_cast<long>(nb) * NT;
-        for (long e = static_cast<long>(blockIdx.x) * NT + threadIdx.x; e < total; e += stride) {
-          const int c = static_cast<int>(e % D);
-          const int k = kFix ? 0 : c;
-          double xv = xs[e];
-          double rv = a.r[e];
-          if (pc.act[c]) {
-            const double alpha = pc.coef[c];
-            xv = xv + alpha * __ldg(pin + e);
-            rv = rv - alpha * __ldg(a.q + e);
-            if (!isfinite(xv)) acc[2][k] += 1.0;
+        for (long e0 = static_cast<long>(blockIdx.x) * NT + threadIdx.x; e0 < total; e0 += U * stride) {
+          double xv[U], rv[U], pv[U], qv[U], iv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long e = e0 + u * stride;
+            if (e < total) {
+              xv[u] = xs[e];
+              rv[u] = a.r[e];
+              pv[u] = __ldg(pin + e);
+              qv[u] = __ldg(a.q + e);
+              iv[u] = __ldg(g.invd + e / D);
+            }
           }
-          const double z = __ldg(g.invd + e / D) * rv;
-          acc[0][k] += rv * rv;
-          acc[1][k] += rv * z;
-          x[e] = xv;
-          a.r[e] = rv;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long e = e0 + u * stride;
+            if (e >= total) break;
+            const int c = static_cast<int>(e % D);
+            const int k = kFix ? 0 : c;
+            if (pc.act[c]) {
+              const double alpha = pc.coef[c];
+              xv[u] = xv[u] + alpha * pv[u];
+              rv[u] = rv[u] - alpha * qv[u];
+              if (!isfinite(xv[u])) acc[2][k] += 1.0;
+            }
+            const double z = iv[u] * rv[u];
+            acc[0][k] += rv[u] * rv[u];
+            acc[1][k] += rv[u] * z;
+            x[e] = xv[u];
+            a.r[e] = rv[u];
+          }
         }
         block_reduce_store<3, D, VA, NT>(acc, a.part);
       }
       grid.sync();
+    PFE_TRACE(5);
       reduce_partials<3, D, NT>(a.part, nb, tot);
       if (threadIdx.x < 32) {  // stop test and beta (pcg.cpp:75-88)
         const int j = threadIdx.x;
@@ -317,6 +390,7 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
     }
     ycur ^= 1;
     grid.sync();
+    PFE_TRACE(6);
 
     // ---------------- split-Bregman pass (solver.cpp:96-98, 83-84)
     {
@@ -377,6 +451,7 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
     ebcur ^= 1;
     b_zero = false;
     grid.sync();
+    PFE_TRACE(8);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.ctl->nonfinite_y, 1);
 }

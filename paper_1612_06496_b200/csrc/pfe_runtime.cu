@@ -37,6 +37,7 @@ using pfe_host::TopoDesc;
 namespace {
 
 thread_local std::string g_last_error;
+constexpr int kTraceCap = 1 << 16;
 
 #define CK(x)                                                                                   \
   do {                                                                                          \
@@ -185,6 +186,7 @@ struct pfe_solver {
   int sm = 148;
   bool use_graphs = true, warn = true;
   bool persistent = true;  // grid topologies: one cooperative launch per split_bregman call
+  unsigned long long* trace = nullptr;  // PFE_TRACE=1: phase trace of the persistent kernel
   pfe_params prm{};
   int n = 0;
   long m = 0;
@@ -351,6 +353,74 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   const double dterm = 0.5 * S->prm.r;
   cudaStream_t st = S->stream;
 
+  auto finish_diag = [&](std::vector<double>& diag) {
+    std::vector<double> invd(n);
+    for (int v = 0; v < n; ++v) {
+      diag[v] += dterm * g.deg[v];  // the (r/2) d_v triplet is summed last
+      invd[v] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[v] > 0.0 ? 1.0 / diag[v] : 1.0);
+    }
+    S->diag = S->mem.upload(diag, st);
+    S->invd = S->mem.upload(invd, st);
+  };
+
+  // grid eligibility: hint consistent, W wide enough for the slot order to be
+  // the column order, edges strictly lexicographic and all stencil offsets.
+  bool grid = gh > 0 && gw > 0 && static_cast<long>(gh) * gw == n && (grad == 1 || grad == 2) &&
+              gw >= 2 * grad + 2;
+  std::vector<long> slot_of;
+  if (grid) {
+    slot_of.resize(static_cast<size_t>(m));
+    const int S_ = grad == 1 ? 4 : 12;
+    for (long k = 0; k < m && grid; ++k) {
+      if (k > 0 && !(g.ei[k - 1] < g.ei[k] || (g.ei[k - 1] == g.ei[k] && g.ej[k - 1] < g.ej[k]))) grid = false;
+      const int s = grid_slot(grad, gw, g.ei[k], g.ej[k]);
+      if (s < 0) grid = false;
+      slot_of[k] = static_cast<long>(g.ei[k]) * S_ + s;
+    }
+  }
+  if (grid) {
+    const int S_ = grad == 1 ? 4 : 12;
+    std::vector<double> wf(static_cast<size_t>(n) * S_, 0.0);
+    for (long k = 0; k < m; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
+    // diag(A)_v: incident edges in edge-index order = backward slots (u
+    // ascending) then forward slots; absent slots hold 0 and add +0.0.
+    std::vector<double> diag(n, 0.0);
+    std::vector<int> off(S_);
+    for (int s = 0; s < S_; ++s) {
+      const int dy = grad == 1 ? (s == 0 ? 0 : 1) : (s < 2 ? 0 : (s < 7 ? 1 : 2));
+      const int dx = grad == 1 ? (s == 0 ? 1 : s - 2) : (s < 2 ? s + 1 : (s < 7 ? s - 4 : s - 9));
+      off[s] = dy * gw + dx;
+    }
+    for (int v = 0; v < n; ++v) {
+      const int y = v / gw, x = v % gw;
+      double acc = 0.0;
+      for (int s = S_ - 1; s >= 0; --s) {
+        const int dy = off[s] >= gw - grad ? (off[s] + grad) / gw : 0, dx = off[s] - dy * gw;
+        const int yy = y - dy, xx = x - dx;
+        if (yy < 0 || xx < 0 || xx >= gw) continue;
+        const double w = wf[static_cast<size_t>(v - off[s]) * S_ + s];
+        acc += (hl * w) * w;
+      }
+      for (int s = 0; s < S_; ++s) {
+        const double w = wf[static_cast<size_t>(v) * S_ + s];
+        acc += (hl * w) * w;
+      }
+      diag[v] = acc;
+    }
+    finish_diag(diag);
+    double* dwf = S->mem.upload(wf, st);
+    S->edge_row = std::move(slot_of);
+    S->edge_rows = static_cast<long>(n) * S_;
+    if (grad == 1) {
+      S->topo.kind = pfe_host::kTopoGrid1;
+      S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd};
+    } else {
+      S->topo.kind = pfe_host::kTopoGrid2;
+      S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd};
+    }
+    return;
+  }
+
   // incidence lists in increasing edge index (the row order of M^T)
   std::vector<int> iptr(static_cast<size_t>(n) + 1, 0);
   for (long k = 0; k < m; ++k) {
@@ -374,48 +444,13 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       iw[at] = g.w[k];
     }
   }
-  std::vector<double> diag(n), invd(n);
+  std::vector<double> diag(n);
   for (int v = 0; v < n; ++v) {
-    double s = 0.0;
-    for (int k = iptr[v]; k < iptr[v + 1]; ++k) s += (hl * iw[k]) * iw[k];
-    s += dterm * g.deg[v];
-    diag[v] = s;
-    invd[v] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (s > 0.0 ? 1.0 / s : 1.0);
+    double acc = 0.0;
+    for (int k = iptr[v]; k < iptr[v + 1]; ++k) acc += (hl * iw[k]) * iw[k];
+    diag[v] = acc;
   }
-  S->diag = S->mem.upload(diag, st);
-  S->invd = S->mem.upload(invd, st);
-
-  // grid eligibility: hint consistent, W wide enough for the slot order to be
-  // the column order, edges strictly lexicographic and all stencil offsets.
-  bool grid = gh > 0 && gw > 0 && static_cast<long>(gh) * gw == n && (grad == 1 || grad == 2) &&
-              gw >= 2 * grad + 2;
-  std::vector<long> slot_of;
-  if (grid) {
-    slot_of.resize(static_cast<size_t>(m));
-    const int S_ = grad == 1 ? 4 : 12;
-    for (long k = 0; k < m && grid; ++k) {
-      if (k > 0 && !(g.ei[k - 1] < g.ei[k] || (g.ei[k - 1] == g.ei[k] && g.ej[k - 1] < g.ej[k]))) grid = false;
-      const int s = grid_slot(grad, gw, g.ei[k], g.ej[k]);
-      if (s < 0) grid = false;
-      slot_of[k] = static_cast<long>(g.ei[k]) * S_ + s;
-    }
-  }
-  if (grid) {
-    const int S_ = grad == 1 ? 4 : 12;
-    std::vector<double> wf(static_cast<size_t>(n) * S_, 0.0);
-    for (long k = 0; k < m; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
-    double* dwf = S->mem.upload(wf, st);
-    S->edge_row = std::move(slot_of);
-    S->edge_rows = static_cast<long>(n) * S_;
-    if (grad == 1) {
-      S->topo.kind = pfe_host::kTopoGrid1;
-      S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd};
-    } else {
-      S->topo.kind = pfe_host::kTopoGrid2;
-      S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd};
-    }
-    return;
-  }
+  finish_diag(diag);
 
   // General CSR: A rows sorted by column with duplicate columns summed in
   // edge order (stable sort), exact zeros dropped, diagonal in place.
@@ -470,6 +505,10 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   S->warn = x ? x->warn != 0 : true;
   S->prof.on = x ? x->profile != 0 : false;
   S->persistent = x ? x->persistent != 0 : true;
+  if (const char* tr = std::getenv("PFE_TRACE"); tr && tr[0] == '1') {
+    S->trace = S->mem.alloc<unsigned long long>(kTraceCap);
+    CK(cudaMemset(S->trace, 0, sizeof(unsigned long long) * kTraceCap));
+  }
   CK(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&S->aux, cudaStreamNonBlocking));
   CK(cudaDeviceGetAttribute(&S->sm, cudaDevAttrMultiProcessorCount, S->device));
@@ -814,6 +853,8 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
       in.ctl = S->ctl;
       in.part = S->partials;
       in.part_b = S->partials_b;
+      in.trace = S->trace;
+      in.trace_cap = S->trace ? kTraceCap : 0;
       S->prof.begin(7, S->stream);
       S->tab->sb_persistent(S->topo, in, S->lv());
       S->prof.end(S->stream);
@@ -1087,6 +1128,16 @@ int pfe_solver_kernel_times(const pfe_solver* s, pfe_kernel_times* out, int rese
 }
 
 double pfe_solver_last_ms(const pfe_solver* s) { return s ? s->last_ms : -1.0; }
+
+int64_t pfe_solver_trace(const pfe_solver* s, uint64_t* out, int64_t cap) {
+  int64_t cnt = 0;
+  const int rc = guarded([&] {
+    if (!s->trace) return;
+    cnt = std::min<int64_t>(cap, kTraceCap);
+    CK(cudaMemcpy(out, s->trace, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost));
+  });
+  return rc == PFE_OK ? cnt : -rc;
+}
 
 int pfe_state_create(pfe_solver* s, const double* y0, pfe_state** out) {
   return guarded([&] {
