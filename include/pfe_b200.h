@@ -199,6 +199,28 @@ int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_id
                         int32_t preconditioner, const pfe_exec* x, double* x_out, int32_t* iterations,
                         int32_t* converged, double* residual, int32_t* jacobi_fallback);
 
+/* Multi-GPU row bands for pixel-grid graphs: one process
+ * per GPU; rank 0 calls pfe_nccl_unique_id and shares the bytes (e.g. via
+ * torch.distributed), then every rank creates its band solver from the SAME
+ * global graph.  The band owns image rows [H*rank/nranks, H*(rank+1)/nranks)
+ * plus an R-row halo exchanged with NCCL send/recv; PCG scalars and TSQR
+ * factors are all-gathered.  pfe_state_create takes the global y0;
+ * pfe_run_soc / pfe_two_stage / pfe_split_bregman run the banded solve
+ * (fixed iteration counts); pfe_state_get(PFE_FIELD_Y) returns the global Y
+ * on every rank.  NCCL is loaded at run time (libnccl.so.2). */
+#define PFE_NCCL_ID_BYTES 128
+/* Host only: band `rank` of `nranks` over `height` rows owns [out[0], out[1])
+ * and stores [out[2], out[3]) (owned rows plus the radius-row halo). */
+int pfe_band_plan(int32_t height, int32_t nranks, int32_t radius, int32_t rank, int32_t* out);
+int pfe_nccl_unique_id(uint8_t* out);
+int pfe_solver_create_band(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, const uint8_t* nccl_id,
+                           int32_t nranks, int32_t rank, pfe_solver** out);
+/* The same banded algorithm with `nbands` bands emulated in this process on
+ * one device (device copies instead of NCCL): validates the decomposition.
+ * mode 0: soc, 1: pfe_two_stage. */
+int pfe_solve_banded(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t nbands, int32_t mode,
+                     const double* y0, double* y_out, pfe_report* rep);
+
 /* objective(M, Y) (solver.cpp:14-17) with M = difference_matrix(g). */
 int pfe_objective(const pfe_graph* g, int32_t d, const double* y, const pfe_exec* x, double* out);
 /* shrink(V, gamma) (solver.cpp:19-25), elementwise on count values. */

@@ -85,6 +85,12 @@ _SIGS = {
     "pfe_objective": (C.c_int, [C.POINTER(pfe_graph), C.c_int32, _D, C.POINTER(pfe_exec), _D]),
     "pfe_shrink": (C.c_int, [C.c_int64, _D, C.c_double, C.POINTER(pfe_exec), _D]),
     "pfe_project_orthogonal": (C.c_int, [C.c_int32, C.c_int32, _D, C.POINTER(pfe_exec), _D]),
+    "pfe_band_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _I]),
+    "pfe_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "pfe_solver_create_band": (C.c_int, [C.POINTER(pfe_graph), C.POINTER(pfe_params), C.POINTER(pfe_exec),
+                                         C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "pfe_solve_banded": (C.c_int, [C.POINTER(pfe_graph), C.POINTER(pfe_params), C.POINTER(pfe_exec), C.c_int32,
+                                   C.c_int32, _D, _D, C.POINTER(pfe_report)]),
     "pfe_d_orthonormalize": (C.c_int, [C.c_int32, C.c_int32, _D, _D, _D]),
     "pfe_random_embedding": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _D, _D]),
     "pfe_kmeans": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_int32, C.c_uint64, C.c_int32, _I]),

@@ -470,3 +470,53 @@ def kmeans(points, k: int, seed: int, max_iter: int = 100) -> np.ndarray:
     lab = np.zeros(n, np.int32)
     _check(N.load().pfe_kmeans(n, d, N.dptr(pc), int(k), int(seed), int(max_iter), N.iptr(lab)))
     return lab
+
+
+# ------------------------------------------------------------ row bands ----
+def band_plan(height: int, nranks: int, radius: int, rank: int) -> Tuple[int, int, int, int]:
+    """Rows owned (r0, r1) and stored (lo, hi) by band `rank` (host only)."""
+    out = np.zeros(4, np.int32)
+    _check(N.load().pfe_band_plan(int(height), int(nranks), int(radius), int(rank), N.iptr(out)))
+    return tuple(int(v) for v in out)
+
+
+def soc_banded(g: WeightedGraph, params: PfeParams, y0, nbands: int, two_stage: bool = False,
+               device: int = 0) -> np.ndarray:
+    """The multi-GPU row-band algorithm with `nbands` bands emulated on one device."""
+    if not g.grid:
+        raise ConfigError("row bands need a pixel-grid graph (grid hint)")
+    y0c = _colmajor(y0, g.n, params.dim)
+    out = np.empty(g.n * params.dim)
+    gc, pc, xc = g.to_c(), params.to_c(), _exec(device, False, False, persistent=False)
+    rep = N.pfe_report()
+    _check(N.load().pfe_solve_banded(C.byref(gc), C.byref(pc), C.byref(xc), int(nbands), 1 if two_stage else 0,
+                                     N.dptr(y0c), N.dptr(out), C.byref(rep)))
+    return _from_colmajor(out, g.n, params.dim)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(N.load().pfe_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class BandSolver(PfeSolver):
+    """One row band of a multi-GPU solve (one process per GPU, NCCL between bands).
+
+    Every rank passes the same global graph and the same NCCL id; make_state
+    takes the global y0 and ``state.y`` returns the global Y on every rank.
+    """
+
+    def __init__(self, graph: WeightedGraph, params: PfeParams, nccl_id: bytes, nranks: int, rank: int,
+                 device: int = 0, warn: bool = True):
+        lib = N.load()
+        self.graph = graph
+        self.params_ = params
+        self._g = graph.to_c()
+        self._p = params.to_c()
+        self._x = _exec(device, False, warn, False, False)
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        _check(lib.pfe_solver_create_band(C.byref(self._g), C.byref(self._p), C.byref(self._x), idbuf, int(nranks),
+                                          int(rank), C.byref(h)))
+        self._h = h

@@ -86,7 +86,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
             list(ex.map(run, cmds))
     newest = max(o.stat().st_mtime for o in objs)
     if not LIB.exists() or LIB.stat().st_mtime < newest:
-        run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+        run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl"])
     return LIB
 
 

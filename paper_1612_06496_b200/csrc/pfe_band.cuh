@@ -1,0 +1,472 @@
+// Row-band decomposition of pixel-grid graphs over several GPUs
+// (DESIGN.md §6).  Included by pfe_runtime.cu inside its
+// anonymous namespace (needs pfe_solver / pfe_state).
+//
+// Band p of P owns global image rows [r0, r1) and stores rows [lo, hi) =
+// [r0 - R, r1 + R) clipped to the image: its owned rows plus an R-row halo
+// (R = stencil radius).  Every kernel processes owned rows only (Grid::row_lo
+// / row_hi); the halo rows are copies refreshed from the neighbouring bands:
+//   * p0 after init, p' after every SpMV and r after every update (the fused
+//     SpMV recomputes p' = D^-1 r + beta p on its halo),
+//   * Y after every result selection (init and the split-Bregman pass read
+//     the neighbours' rows).
+// split_b / split_s of an edge crossing a band boundary are replicated in both
+// bands: the lower band updates its copy with exactly the arithmetic the
+// owning band uses, so no edge data is ever exchanged.  PCG reductions: each
+// band reduces its block partials to d or 3d totals, the totals of all bands
+// are gathered, and every band sums them in rank order, so all bands take
+// identical alpha / beta / stop decisions.  The TSQR factors of all bands are
+// gathered the same way before the d x d polar step.
+//
+// Transport: bands in separate processes (one GPU each) use NCCL send/recv
+// for halos and all-gathers for totals (loaded at run time from
+// libnccl.so.2); bands emulated inside one process (pfe_solve_banded, used to
+// validate the decomposition on one GPU) use device-to-device copies.
+
+struct BandPlan {
+  int r0, r1, lo, hi;
+};
+
+BandPlan band_plan(int H, int P, int R, int p) {
+  const int r0 = static_cast<int>(static_cast<long>(H) * p / P);
+  const int r1 = static_cast<int>(static_cast<long>(H) * (p + 1) / P);
+  return {r0, r1, p > 0 ? std::max(0, r0 - R) : r0, p < P - 1 ? std::min(H, r1 + R) : r1};
+}
+
+// ------------------------------------------------------------------ NCCL --
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.h) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) config_error(std::string("multi-GPU row bands need NCCL: ") + dlerror());
+  auto sym = [&](const char* name) {
+    void* f = dlsym(h, name);
+    if (!f) config_error(std::string("NCCL symbol missing: ") + name);
+    return f;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.h = h;
+  g_comm_destroy = [](void* c) { nccl().CommDestroy(static_cast<ncclComm_t>(c)); };
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(PFE_CUDA_ERROR, std::string(what) + " failed: " + nccl().GetErrorString(r));
+}
+
+// ------------------------------------------------------ band construction --
+// Global slot weights -> this band's rows; diag(A) and its inverse are taken
+// from the GLOBAL graph (halo vertices have edges outside the band).
+void setup_band_grid(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad, const BandPlan& bp) {
+  const int S_ = grad == 1 ? 4 : 12;
+  if (!(gh > 0 && gw > 0 && static_cast<long>(gh) * gw == g.n && (grad == 1 || grad == 2) && gw >= 2 * grad + 2))
+    config_error("row bands need a pixel-grid graph (grid_h * grid_w == n, radius 1 or 2)");
+  const double hl = 0.5 * S->prm.lambda, dterm = 0.5 * S->prm.r;
+  std::vector<double> wf(static_cast<size_t>(g.n) * S_, 0.0);
+  for (long k = 0; k < g.m; ++k) {
+    if (k > 0 && !(g.ei[k - 1] < g.ei[k] || (g.ei[k - 1] == g.ei[k] && g.ej[k - 1] < g.ej[k])))
+      config_error("row bands need lexicographically ordered grid edges");
+    const int s = grid_slot(grad, gw, g.ei[k], g.ej[k]);
+    if (s < 0) config_error("row bands: edge " + std::to_string(k) + " is not a stencil neighbour");
+    wf[static_cast<size_t>(g.ei[k]) * S_ + s] = g.w[k];
+  }
+  const long vb = static_cast<long>(bp.lo) * gw, ve = static_cast<long>(bp.hi) * gw, nl = ve - vb;
+  std::vector<double> wl(wf.begin() + vb * S_, wf.begin() + ve * S_);
+  std::vector<double> diag(nl), invd(nl), deg(nl), sqd(nl);
+  for (long v = vb; v < ve; ++v) {
+    const int y = static_cast<int>(v / gw), x = static_cast<int>(v % gw);
+    double acc = 0.0;
+    for (int s = S_ - 1; s >= 0; --s) {  // backward slots (u ascending)
+      const int dy = grad == 1 ? (s == 0 ? 0 : 1) : (s < 2 ? 0 : (s < 7 ? 1 : 2));
+      const int dx = grad == 1 ? (s == 0 ? 1 : s - 2) : (s < 2 ? s + 1 : (s < 7 ? s - 4 : s - 9));
+      const int yy = y - dy, xx = x - dx;
+      if (yy < 0 || xx < 0 || xx >= gw) continue;
+      const double w = wf[static_cast<size_t>(static_cast<long>(yy) * gw + xx) * S_ + s];
+      acc += (hl * w) * w;
+    }
+    for (int s = 0; s < S_; ++s) {
+      const double w = wf[static_cast<size_t>(v) * S_ + s];
+      acc += (hl * w) * w;
+    }
+    const long l = v - vb;
+    diag[l] = acc + dterm * g.deg[v];
+    invd[l] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[l] > 0.0 ? 1.0 / diag[l] : 1.0);
+    deg[l] = g.deg[v];
+    sqd[l] = std::sqrt(g.deg[v]);
+  }
+  S->n = static_cast<int>(nl);
+  S->deg = S->mem.upload(deg, S->stream);
+  S->sqd = S->mem.upload(sqd, S->stream);
+  S->diag = S->mem.upload(diag, S->stream);
+  S->invd = S->mem.upload(invd, S->stream);
+  double* dwf = S->mem.upload(wl, S->stream);
+  S->row_lo = bp.r0 - bp.lo;
+  S->row_hi = bp.r1 - bp.lo;
+  S->band_h = gh;
+  S->band_w = gw;
+  S->band_rad = grad;
+  S->band_r0 = bp.r0;
+  S->band_r1 = bp.r1;
+  S->band_lo = bp.lo;
+  S->edge_rows = nl * S_;
+  const int hloc = bp.hi - bp.lo;
+  if (grad == 1) {
+    S->topo.kind = pfe_host::kTopoGrid1;
+    S->topo.g1 = pfe_dev::Grid<1>{S->n, hloc, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+  } else {
+    S->topo.kind = pfe_host::kTopoGrid2;
+    S->topo.g2 = pfe_dev::Grid<2>{S->n, hloc, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+  }
+}
+
+pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int nranks, int rank,
+                               void* comm) {
+  if (!g || !p) config_error("null graph or params");
+  const auto t0 = std::chrono::steady_clock::now();
+  HostGraph hg{g->n, static_cast<long>(g->m), g->ei, g->ej, g->w, g->degree};
+  validate(hg, *p, true);
+  const int R = g->grid_radius;
+  if (nranks < 1 || rank < 0 || rank >= nranks) config_error("row bands: bad rank / rank count");
+  if (g->grid_h / nranks < std::max(R, 1)) config_error("row bands: every band needs at least R image rows");
+  auto S = std::make_unique<pfe_solver>();
+  S->prm = *p;
+  S->jacobi_fallback = p->preconditioner == PFE_PRECOND_IC0;
+  init_common(S.get(), x, p->dim);
+  S->persistent = false;  // grid-wide barriers cannot span GPUs
+  S->use_graphs = false;
+  S->nranks = nranks;
+  S->rank = rank;
+  S->comm = comm;
+  S->m = g->m;
+  S->global_n = g->n;
+  const BandPlan bp = band_plan(g->grid_h, nranks, R, rank);
+  setup_band_grid(S.get(), hg, g->grid_h, g->grid_w, R, bp);
+  int maxrows = 0;
+  for (int q = 0; q < nranks; ++q) {
+    const BandPlan b = band_plan(g->grid_h, nranks, R, q);
+    maxrows = std::max(maxrows, b.r1 - b.r0);
+  }
+  S->band_maxrows = maxrows;
+  const int d = S->d;
+  S->qr_blocks = qr_blocks_for(S.get(), static_cast<long>(maxrows) * g->grid_w);  // equal on every band
+  S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * d * d);
+  S->rgather = S->mem.alloc<double>(static_cast<size_t>(nranks) * S->qr_blocks * d * d);
+  S->wmat = S->mem.alloc<double>(static_cast<size_t>(d) * d);
+  S->tot_local = S->mem.alloc<double>(3 * pfe_dev::kMaxD);
+  S->gathered_a = S->mem.alloc<double>(static_cast<size_t>(nranks) * 3 * d);
+  S->gathered_b = S->mem.alloc<double>(static_cast<size_t>(nranks) * d);
+  const size_t rows = static_cast<size_t>(maxrows) * g->grid_w * d;
+  S->ystage = S->mem.alloc<double>(rows);
+  S->yall = S->mem.alloc<double>(rows * nranks);
+  S->ensure_log(64);
+  CK(cudaStreamSynchronize(S->stream));
+  S->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return S.release();
+}
+
+// Band state: y0 is the GLOBAL column-major n x d embedding.
+pfe_state* create_band_state(pfe_solver* S, const double* y0_global) {
+  const long gn = S->global_n, vb = static_cast<long>(S->band_lo) * S->band_w;
+  std::vector<double> loc(static_cast<size_t>(S->n) * S->d);
+  for (int j = 0; j < S->d; ++j)
+    std::memcpy(loc.data() + static_cast<size_t>(j) * S->n, y0_global + j * gn + vb, sizeof(double) * S->n);
+  return create_state(S, loc.data());
+}
+
+// ------------------------------------------------------------------ team --
+struct Team {
+  std::vector<pfe_state*> st;  // one band (NCCL) or every band (emulated)
+  bool emulated = false;
+  pfe_solver* S(size_t i) const { return st[i]->s; }
+  size_t size() const { return st.size(); }
+};
+
+void team_sync(Team& t) {
+  for (auto* st : t.st) CK(cudaStreamSynchronize(st->s->stream));
+}
+
+// Per-band totals of the producer's partials, then the totals of all bands.
+void team_gather_totals(Team& t, int nq, bool spmv_partials, int nb_producer_of(const pfe_solver*, bool)) {
+  const int d = t.S(0)->d, P = t.S(0)->nranks;
+  const size_t cnt = static_cast<size_t>(nq) * d;
+  for (auto* st : t.st) {
+    pfe_solver* S = st->s;
+    S->tab->local_totals(nq, spmv_partials ? S->partials_b : S->partials, nb_producer_of(S, spmv_partials),
+                         S->tot_local, S->stream);
+  }
+  if (t.emulated) {
+    team_sync(t);
+    for (size_t j = 0; j < t.size(); ++j)
+      for (size_t i = 0; i < t.size(); ++i) {
+        double* dst = (spmv_partials ? t.S(j)->gathered_b : t.S(j)->gathered_a) + i * cnt;
+        CK(cudaMemcpy(dst, t.S(i)->tot_local, sizeof(double) * cnt, cudaMemcpyDeviceToDevice));
+      }
+    return;
+  }
+  pfe_solver* S = t.S(0);
+  (void)P;
+  nccl_check(nccl().AllGather(S->tot_local, spmv_partials ? S->gathered_b : S->gathered_a, cnt, ncclDouble,
+                              static_cast<ncclComm_t>(S->comm), S->stream),
+             "ncclAllGather(totals)");
+}
+
+// Refreshes the R halo rows of `field` (a [n_local][d] array) from the
+// neighbouring bands.
+template <class F>
+void team_halo(Team& t, F&& field) {
+  const pfe_solver* S0 = t.S(0);
+  const int d = S0->d, R = S0->band_rad, W = S0->band_w;
+  const size_t blk = static_cast<size_t>(R) * W * d;  // doubles per halo block
+  auto rows = [&](pfe_state* st, int local_row) { return field(st) + static_cast<size_t>(local_row) * W * d; };
+  if (t.emulated) {
+    team_sync(t);
+    for (size_t p = 1; p < t.size(); ++p) {
+      pfe_state* up = t.st[p - 1];
+      pfe_state* dn = t.st[p];
+      // dn's top owned rows -> up's bottom halo; up's bottom owned rows -> dn's top halo
+      CK(cudaMemcpy(rows(up, up->s->row_hi), rows(dn, dn->s->row_lo), sizeof(double) * blk,
+                    cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpy(rows(dn, 0), rows(up, up->s->row_hi - R), sizeof(double) * blk, cudaMemcpyDeviceToDevice));
+    }
+    return;
+  }
+  pfe_state* st = t.st[0];
+  pfe_solver* S = st->s;
+  auto comm = static_cast<ncclComm_t>(S->comm);
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  if (S->rank > 0) {
+    nccl_check(nccl().Send(rows(st, S->row_lo), blk, ncclDouble, S->rank - 1, comm, S->stream), "ncclSend");
+    nccl_check(nccl().Recv(rows(st, 0), blk, ncclDouble, S->rank - 1, comm, S->stream), "ncclRecv");
+  }
+  if (S->rank < S->nranks - 1) {
+    nccl_check(nccl().Send(rows(st, S->row_hi - R), blk, ncclDouble, S->rank + 1, comm, S->stream), "ncclSend");
+    nccl_check(nccl().Recv(rows(st, S->row_hi), blk, ncclDouble, S->rank + 1, comm, S->stream), "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+}
+
+int nb_producer(const pfe_solver* S, bool spmv) {
+  int nb_init = 0, nb_spmv = 0, nb_update = 0;
+  S->tab->pcg_grids(S->topo, S->lv(), &nb_init, &nb_spmv, &nb_update);
+  return spmv ? nb_spmv : nb_update;
+}
+int nb_producer_init(const pfe_solver* S, bool) {
+  int nb_init = 0, nb_spmv = 0, nb_update = 0;
+  S->tab->pcg_grids(S->topo, S->lv(), &nb_init, &nb_spmv, &nb_update);
+  return nb_init;
+}
+
+// One PCG solve of every band (pcg.cpp:40-114 for all d columns).
+void team_pcg(Team& t, const std::vector<const double*>& rhs) {
+  const size_t B = t.size();
+  std::vector<PcgArgs> a(B);
+  for (size_t i = 0; i < B; ++i) {
+    pfe_solver* S = t.S(i);
+    a[i] = pcg_args(t.st[i], rhs[i]);
+    a[i].rd_a = S->gathered_a;
+    a[i].rd_b = S->gathered_b;
+    a[i].rank_major = 1;
+    a[i].nb_init = a[i].nb_update = a[i].nb_spmv = S->nranks;
+  }
+  const int maxit = t.S(0)->prm.pcg_max_iter;
+  for (size_t i = 0; i < B; ++i) t.S(i)->tab->pcg_init(t.S(i)->topo, a[i], t.S(i)->lv());
+  team_gather_totals(t, 3, false, nb_producer_init);
+  team_halo(t, [](pfe_state* st) { return st->pb[0]; });
+  auto spmv = [&](int k) {
+    for (size_t i = 0; i < B; ++i) {
+      a[i].phase = pfe_dev::pcg_phase(k);
+      t.S(i)->tab->pcg_spmv(t.S(i)->topo, a[i], t.S(i)->lv());
+    }
+    team_gather_totals(t, 1, true, nb_producer);
+  };
+  int k = 1;
+  spmv(1);
+  for (;;) {
+    pfe_solver* S0 = t.S(0);
+    S0->read_ctl();  // every band took the same decision
+    if (!S0->h_ctl->any_active || k > maxit) break;
+    if (k > 1) team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
+    for (size_t i = 0; i < B; ++i) {
+      a[i].phase = pfe_dev::pcg_phase(k);
+      t.S(i)->tab->pcg_update(t.S(i)->topo, a[i], t.S(i)->lv());
+    }
+    team_gather_totals(t, 3, false, nb_producer);
+    team_halo(t, [](pfe_state* st) { return st->r; });
+    spmv(++k);
+  }
+  for (size_t i = 0; i < B; ++i) {
+    pfe_state* st = t.st[i];
+    pfe_solver* S = st->s;
+    const long vb = static_cast<long>(S->row_lo) * S->band_w * S->d;
+    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    S->tab->pcg_finalize(cnt, st->y + vb, st->y2 + vb, S->ctl, {S->grid_for(static_cast<long>(cnt) * S->d), S->stream, S->sm});
+    ++S->inner_launched;
+    std::swap(st->y, st->y2);
+  }
+  team_halo(t, [](pfe_state* st) { return st->y; });
+}
+
+// PfeSolver::split_bregman (solver.cpp:73-108) over every band.
+void team_split_bregman(Team& t, int max_iter) {
+  const size_t B = t.size();
+  std::vector<const double*> rhs(B);
+  for (size_t i = 0; i < B; ++i) {
+    pfe_state* st = t.st[i];
+    pfe_solver* S = st->s;
+    const long vb = static_cast<long>(S->row_lo) * S->band_w;
+    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    if (!st->rq_valid) {
+      S->tab->rhs_quad(cnt, S->sqd + vb, st->p + vb * S->d, st->breg + vb * S->d, st->rq + vb * S->d,
+                       0.5 * S->prm.r, {S->grid_for(static_cast<long>(cnt) * S->d), S->stream, S->sm});
+      st->rq_valid = true;
+    }
+    rhs[i] = st->rq;
+    if (!st->inner_zero) {
+      S->tab->rhs_from_state(S->topo, st->es, st->eb[st->eb_cur], st->rq, st->r, 0.5 * S->prm.lambda, S->lv());
+      rhs[i] = st->r;
+    }
+  }
+  for (int it = 0; it < max_iter; ++it) {
+    const bool last = it == max_iter - 1;
+    team_pcg(t, rhs);
+    for (size_t i = 0; i < B; ++i) {
+      pfe_state* st = t.st[i];
+      pfe_solver* S = st->s;
+      SbArgs sa{};
+      sa.y = st->y;
+      sa.b_old = st->inner_zero ? nullptr : st->eb[st->eb_cur];
+      sa.b_new = st->eb[st->eb_cur ^ 1];
+      sa.s_out = last ? st->es : nullptr;
+      sa.rq = st->rq;
+      sa.rhs = last ? nullptr : st->r;
+      sa.hl = 0.5 * S->prm.lambda;
+      sa.gamma = 1.0 / S->prm.lambda;
+      sa.ctl = S->ctl;
+      S->tab->sb_pass(S->topo, sa, S->lv());
+      st->eb_cur ^= 1;
+      st->inner_zero = false;
+      rhs[i] = st->r;
+    }
+  }
+}
+
+// Projection (solver.cpp:116-118): TSQR factors of every band folded in rank
+// order on every band, so all bands apply the same W.
+void team_project(Team& t) {
+  const size_t B = t.size();
+  const int d = t.S(0)->d;
+  const size_t fac = static_cast<size_t>(t.S(0)->qr_blocks) * d * d;
+  for (size_t i = 0; i < B; ++i) {
+    pfe_state* st = t.st[i];
+    pfe_solver* S = st->s;
+    const long vb = static_cast<long>(S->row_lo) * S->band_w;
+    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    S->tab->tsqr_local(cnt, st->y + vb * d, S->sqd + vb, st->breg + vb * d, S->rbuf, {S->qr_blocks, S->stream, S->sm});
+  }
+  if (t.emulated) {
+    team_sync(t);
+    for (size_t j = 0; j < B; ++j)
+      for (size_t i = 0; i < B; ++i)
+        CK(cudaMemcpy(t.S(j)->rgather + i * fac, t.S(i)->rbuf, sizeof(double) * fac, cudaMemcpyDeviceToDevice));
+  } else {
+    pfe_solver* S = t.S(0);
+    nccl_check(nccl().AllGather(S->rbuf, S->rgather, fac, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
+               "ncclAllGather(R factors)");
+  }
+  for (size_t i = 0; i < B; ++i) {
+    pfe_state* st = t.st[i];
+    pfe_solver* S = st->s;
+    const long vb = static_cast<long>(S->row_lo) * S->band_w;
+    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    S->tab->tsqr_final(S->nranks * S->qr_blocks, S->rgather, S->wmat, S->ctl, {1, S->stream, S->sm});
+    S->tab->project_apply(cnt, st->y + vb * d, S->sqd + vb, st->breg + vb * d, S->wmat, st->p + vb * d,
+                          st->rq + vb * d, 0.5 * S->prm.r, {S->grid_for(cnt), S->stream, S->sm});
+    st->rq_valid = true;
+  }
+}
+
+void team_check(Team& t) {
+  for (auto* st : t.st) check_flags(st->s);
+}
+
+// PfeSolver::run_soc (solver.cpp:110-126) over every band (fixed counts;
+// the relative-change test is not supported across bands).
+void team_run_soc(Team& t, int soc_max, int sb_max) {
+  for (auto* st : t.st) st->s->ensure_log(static_cast<long>(soc_max) * sb_max);
+  for (int k = 0; k < soc_max; ++k) {
+    for (auto* st : t.st) st->inner_zero = true;
+    team_split_bregman(t, sb_max);
+    team_project(t);
+    team_check(t);
+  }
+}
+
+// Global column-major Y from the owned rows of every band.
+void team_gather_y(Team& t, double* out) {
+  const pfe_solver* S0 = t.S(0);
+  const int d = S0->d, W = S0->band_w, P = S0->nranks;
+  const long gn = S0->global_n;
+  const size_t slot = static_cast<size_t>(S0->band_maxrows) * W * d;
+  std::vector<double> all;
+  if (t.emulated) {
+    all.assign(slot * P, 0.0);
+    for (size_t i = 0; i < t.size(); ++i) {
+      const pfe_solver* S = t.S(i);
+      const size_t cnt = static_cast<size_t>(S->row_hi - S->row_lo) * W * d;
+      CK(cudaMemcpy(all.data() + i * slot, t.st[i]->y + static_cast<size_t>(S->row_lo) * W * d, sizeof(double) * cnt,
+                    cudaMemcpyDeviceToHost));
+    }
+  } else {
+    pfe_state* st = t.st[0];
+    pfe_solver* S = st->s;
+    const size_t cnt = static_cast<size_t>(S->row_hi - S->row_lo) * W * d;
+    CK(cudaMemcpyAsync(S->ystage, st->y + static_cast<size_t>(S->row_lo) * W * d, sizeof(double) * cnt,
+                       cudaMemcpyDeviceToDevice, S->stream));
+    nccl_check(nccl().AllGather(S->ystage, S->yall, slot, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
+               "ncclAllGather(Y)");
+    all.resize(slot * P);
+    CK(cudaMemcpyAsync(all.data(), S->yall, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, S->stream));
+    CK(cudaStreamSynchronize(S->stream));
+  }
+  for (int p = 0; p < P; ++p) {
+    const BandPlan bp = band_plan(S0->band_h, P, S0->band_rad, p);
+    const long v0 = static_cast<long>(bp.r0) * W, cnt = static_cast<long>(bp.r1 - bp.r0) * W;
+    for (long v = 0; v < cnt; ++v)
+      for (int j = 0; j < d; ++j) out[(v0 + v) + j * gn] = all[p * slot + static_cast<size_t>(v) * d + j];
+  }
+}
+
+// Device time of a band call (CUDA events on the band's stream).
+template <class F>
+void band_timed(pfe_solver* S, F&& f) {
+  CK(cudaEventRecord(S->ev0, S->stream));
+  f();
+  CK(cudaEventRecord(S->ev1, S->stream));
+  CK(cudaEventSynchronize(S->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+  S->last_ms = ms;
+}

@@ -158,7 +158,13 @@ struct Grid {
   const double* __restrict__ wf;        // [n][S]
   const double* __restrict__ diag;      // A_vv
   const double* __restrict__ invd;      // Jacobi
+  // Rows whose vertices this solver owns (outputs and reductions); the rows
+  // outside [row_lo, row_hi) are a halo copied from neighbouring row bands.
+  // A single-GPU solver owns every row.
+  int row_lo, row_hi;
   __device__ __forceinline__ double inv_diag(int v) const { return __ldg(invd + v); }
+  __device__ __forceinline__ int vbeg() const { return row_lo * W; }
+  __device__ __forceinline__ int vend() const { return row_hi * W; }
 
   template <class F>
   __device__ __forceinline__ void visitE(int v, F&& f) const {
@@ -225,7 +231,10 @@ struct Csr {
   const int* __restrict__ ieid;
   const double* __restrict__ iw;
   const double* __restrict__ invd;
+  int vb, ve;  // owned vertex range
   __device__ __forceinline__ double inv_diag(int v) const { return __ldg(invd + v); }
+  __device__ __forceinline__ int vbeg() const { return vb; }
+  __device__ __forceinline__ int vend() const { return ve; }
 
   template <class F>
   __device__ __forceinline__ void visitA(int v, F&& f) const {

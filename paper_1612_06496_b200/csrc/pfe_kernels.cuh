@@ -39,6 +39,8 @@ struct PcgArgs {
   Ctl* ctl;
   double* part_a;      // partials of init / update (3 x D pairs, pair-major)
   double* part_b;      // partials of spmv (D pairs)
+  const double* rd_a;  // what the consumers reduce: part_a / part_b, or the
+  const double* rd_b;  // per-rank totals gathered from every row band
   int nb_init;         // block counts of the producers (consumers reduce that many)
   int nb_update;
   int nb_spmv;
@@ -51,6 +53,9 @@ struct PcgArgs {
   // x read from x0), 1 = odd iteration >= 3 (p' -> pbuf[0], p_old = pbuf[1]),
   // 2 = even iteration (p' -> pbuf[1], p_old = pbuf[0]).
   int phase;
+  // Row-band solvers: part_a / part_b hold the per-rank totals gathered from
+  // every band ([rank][pair], nb = ranks) instead of this grid's block partials.
+  int rank_major;
 };
 
 __host__ __device__ __forceinline__ int pcg_phase(int it) { return it == 1 ? 0 : ((it & 1) ? 1 : 2); }
@@ -62,7 +67,8 @@ constexpr double kInf = __builtin_huge_val();
 // Block-wide fixed-order reduction of a producer's pair-major partials
 // (nb blocks x NQ*D pairs) into shared out[NQ][D]; all NT threads take part.
 template <int NQ, int D, int NT>
-__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nb, double (&out)[NQ][D]) {
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int nb, double (&out)[NQ][D],
+                                                bool rank_major = false) {
   constexpr int P = NQ * D;
   constexpr int CH = P < 16 ? P : 16;
   __shared__ double wsum[NT / 32][CH];
@@ -74,7 +80,8 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ part,
     for (int b = threadIdx.x; b < nb; b += NT) {
 #pragma unroll
       for (int k = 0; k < CH; ++k)
-        if (base + k < P) acc[k] += __ldcg(part + static_cast<long>(base + k) * nb + b);
+        if (base + k < P)
+          acc[k] += __ldcg(part + (rank_major ? static_cast<long>(b) * P + base + k : static_cast<long>(base + k) * nb + b));
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1)
@@ -114,7 +121,7 @@ template <int D, int NT>
 __device__ __forceinline__ bool spmv_prologue(const PcgArgs& a, ColView<D>& cv) {
   __shared__ double tot[3][D];
   const bool first = a.phase == 0;
-  reduce_partials<3, D, NT>(a.part_a, first ? a.nb_init : a.nb_update, tot);
+  reduce_partials<3, D, NT>(a.rd_a, first ? a.nb_init : a.nb_update, tot, a.rank_major != 0);
   if (threadIdx.x < 32) {
     const int j = threadIdx.x;
     const int done = a.ctl->iter;  // PCG iterations completed so far
@@ -182,7 +189,7 @@ __device__ __forceinline__ bool update_prologue(const PcgArgs& a, ColView<D>& cv
   __shared__ double tot[1][D];
   const int active = a.ctl->any_active;  // written by this iteration's SpMV
   if (!active) return false;             // uniform across the grid
-  reduce_partials<1, D, NT>(a.part_b, a.nb_spmv, tot);
+  reduce_partials<1, D, NT>(a.rd_b, a.nb_spmv, tot, a.rank_major != 0);
   if (threadIdx.x < 32) {
     const int j = threadIdx.x;
     bool act = false;
@@ -221,9 +228,9 @@ template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   double acc[3][V] = {};
-  const long total = static_cast<long>(topo.n) * TPV;
+  const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double ax[V] = {};
@@ -263,9 +270,9 @@ __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
   double* pnew = pcg_pnew(a);
   const double* pold = pcg_pold(a);
   double acc[1][V] = {};
-  const long total = static_cast<long>(topo.n) * TPV;
+  const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double q[V] = {};
@@ -316,9 +323,9 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
   const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
   const double* xsrc = a.phase == 0 ? a.x0 : a.x;
   const double* pin = pcg_pnew(a);
-  const long total = static_cast<long>(topo.n) * TPV;
+  const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   // first item's data is loaded before the prologue's reduction so both
   // memory round trips overlap
   Row<V> x{}, r{}, p{}, q{};
@@ -405,6 +412,16 @@ __global__ void __launch_bounds__(kBlock) k_pcg_finalize(int n, const double* __
   }
 }
 
+// Reduces one grid's block partials (pair-major, nb blocks) to NQ*D totals;
+// row-band solvers then gather these totals from every band so all bands
+// derive the same PCG scalars (reduced in rank order).
+template <int NQ, int D>
+__global__ void __launch_bounds__(kBlock) k_local_totals(const double* part, int nb, double* out) {
+  __shared__ double tot[NQ][D];
+  reduce_partials<NQ, D, kBlock>(part, nb, tot);
+  if (threadIdx.x < NQ * D) out[threadIdx.x] = tot[threadIdx.x / D][threadIdx.x % D];
+}
+
 // ----------------------------------------------------- split-Bregman pass ---
 struct SbArgs {
   const double* y;      // new Y
@@ -427,10 +444,10 @@ struct SbArgs {
 template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock) k_sb_pass(Topo topo, SbArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
-  const long total = static_cast<long>(topo.n) * TPV;
+  const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   int bad = 0;
-  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     const Row<V> yv = ldg_row<V>(a.y + static_cast<long>(v) * D + c0);
@@ -482,9 +499,9 @@ __global__ void __launch_bounds__(kBlock) k_rhs_from_state(Topo topo, const doub
                                                           const double* __restrict__ b,
                                                           const double* __restrict__ rq, double* rhs, double hl) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
-  const long total = static_cast<long>(topo.n) * TPV;
+  const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double acc[V] = {};
@@ -521,9 +538,9 @@ __global__ void __launch_bounds__(kBlock) k_objective(Topo topo, const double* _
                                                      Ctl* ctl) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   double acc[1][V] = {};
-  const long total = static_cast<long>(topo.n) * TPV;
+  const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     const Row<V> yv = ldg_row<V>(y + static_cast<long>(v) * D + c0);

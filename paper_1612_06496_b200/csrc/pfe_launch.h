@@ -75,6 +75,8 @@ struct LaunchTable {
   // Persistent cooperative split-Bregman kernel (grid topologies only).
   // Returns false when the topology has no persistent kernel.
   bool (*sb_persistent)(const TopoDesc&, const PersistIn&, Launch);
+  // block partials -> nq * D totals (nq = 1 or 3), one block
+  void (*local_totals)(int nq, const double* part, int nb, double* out, cudaStream_t);
 };
 
 const LaunchTable& table_for(int d);  // d in [1, 16]

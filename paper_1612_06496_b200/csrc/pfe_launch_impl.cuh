@@ -194,6 +194,13 @@ struct Impl {
     if (t.kind == kTopoGrid2) return persist_grid<2>(t.g2, in, l);
     return false;
   }
+  static void local_totals(int nq, const double* part, int nb, double* out, cudaStream_t s) {
+    if (nq == 3)
+      k_local_totals<3, D><<<1, kBlock, 0, s>>>(part, nb, out);
+    else
+      k_local_totals<1, D><<<1, kBlock, 0, s>>>(part, nb, out);
+    PFE_LAUNCHED(__func__);
+  }
   static int max_blocks_per_sm() {
     int worst = 8, nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_spmv<D, Csr>, kBlock, 0);
@@ -222,7 +229,8 @@ LaunchTable make_table() {
                      &I::tsqr_final,
                      &I::project_apply,
                      &I::max_blocks_per_sm,
-                     &I::sb_persistent};
+                     &I::sb_persistent,
+                     &I::local_totals};
 }
 
 }  // namespace pfe_host

@@ -8,6 +8,8 @@
 // device-side conditional WHILE node, so a whole soc / two_stage run is one
 // graph launch with no host round trips.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -180,12 +182,29 @@ struct GraphCache {
 }  // namespace
 
 // ============================================================== solver ====
+// Set when NCCL is loaded (row-band solvers own a communicator).
+static void (*g_comm_destroy)(void*) = nullptr;
+
 struct pfe_solver {
   int device = 0;
   cudaStream_t stream = nullptr, aux = nullptr;
   int sm = 148;
   bool use_graphs = true, warn = true;
   bool persistent = true;  // grid topologies: one cooperative launch per split_bregman call
+  int row_lo = 0, row_hi = -1;  // owned rows of a row-band solver (-1: every row)
+  // Row-band (multi-GPU) solver: this solver owns global image rows
+  // [band_r0, band_r1) of a band_h x band_w grid and stores local rows
+  // [band_lo, band_lo + H_local) (owned rows plus an R-row halo).
+  int nranks = 1, rank = 0;
+  int band_h = 0, band_w = 0, band_rad = 0, band_r0 = 0, band_r1 = 0, band_lo = 0, band_maxrows = 0;
+  long global_n = 0;
+  void* comm = nullptr;           // ncclComm_t when bands run in separate processes
+  double* tot_local = nullptr;    // [3 d] this band's totals
+  double* gathered_a = nullptr;   // [ranks][3 d]
+  double* gathered_b = nullptr;   // [ranks][d]
+  double* rgather = nullptr;      // [ranks * qr_blocks][d][d] TSQR factors of every band
+  double* ystage = nullptr;       // [band_maxrows * band_w][d] owned-row staging for gathers
+  double* yall = nullptr;         // [ranks][band_maxrows * band_w][d]
   unsigned long long* trace = nullptr;  // PFE_TRACE=1: phase trace of the persistent kernel
   pfe_params prm{};
   int n = 0;
@@ -218,6 +237,7 @@ struct pfe_solver {
   double last_ms = 0.0;  // device time of the last split_bregman / run_soc / two_stage call
 
   ~pfe_solver() {
+    if (comm && g_comm_destroy) g_comm_destroy(comm);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -380,6 +400,10 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
   if (grid) {
     const int S_ = grad == 1 ? 4 : 12;
+    if (S->row_hi < 0) {
+      S->row_lo = 0;
+      S->row_hi = gh;
+    }
     std::vector<double> wf(static_cast<size_t>(n) * S_, 0.0);
     for (long k = 0; k < m; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
     // diag(A)_v: incident edges in edge-index order = backward slots (u
@@ -413,10 +437,10 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     S->edge_rows = static_cast<long>(n) * S_;
     if (grad == 1) {
       S->topo.kind = pfe_host::kTopoGrid1;
-      S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd};
+      S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
     } else {
       S->topo.kind = pfe_host::kTopoGrid2;
-      S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd};
+      S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
     }
     return;
   }
@@ -486,6 +510,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   S->edge_rows = m;
   pfe_dev::Csr c{};
   c.n = n;
+  c.vb = 0;
+  c.ve = n;
   c.aptr = S->mem.upload(aptr, st);
   c.acol = S->mem.upload(acol, st);
   c.aval = S->mem.upload(aval, st);
@@ -666,6 +692,9 @@ PcgArgs pcg_args(pfe_state* st, const double* rhs) {
   a.ctl = S->ctl;
   a.part_a = S->partials;
   a.part_b = S->partials_b;
+  a.rd_a = S->partials;
+  a.rd_b = S->partials_b;
+  a.rank_major = 0;
   S->tab->pcg_grids(S->topo, S->lv(), &a.nb_init, &a.nb_spmv, &a.nb_update);
   a.tol = S->prm.pcg_rel_tol;
   a.max_iter = S->prm.pcg_max_iter;
@@ -1026,6 +1055,8 @@ void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, v
   check_flags(S);
 }
 
+#include "pfe_band.cuh"
+
 }  // namespace
 
 // ================================================================ C ABI ===
@@ -1143,7 +1174,7 @@ int pfe_state_create(pfe_solver* s, const double* y0, pfe_state** out) {
   return guarded([&] {
     if (!y0) config_error("PfeSolver: initial embedding has wrong shape");
     CK(cudaSetDevice(s->device));
-    *out = create_state(s, y0);
+    *out = s->band_w ? create_band_state(s, y0) : create_state(s, y0);
   });
 }
 
@@ -1161,6 +1192,12 @@ int pfe_state_get(pfe_state* st, int32_t field, double* out) {
     pfe_solver* S = st->s;
     CK(cudaSetDevice(S->device));
     const int d = S->d;
+    if (S->band_w) {  // row-band solver: the global Y, gathered from every band
+      if (field != PFE_FIELD_Y) config_error("row-band solvers expose the gathered embedding Y only");
+      Team t{{st}, false};
+      team_gather_y(t, out);
+      return;
+    }
     if (field <= PFE_FIELD_BREGMAN) {
       const double* src = field == PFE_FIELD_Y ? st->y : (field == PFE_FIELD_P ? st->p : st->breg);
       download_rows(S, src, S->n, d, out, st->q);
@@ -1185,6 +1222,7 @@ int pfe_state_set(pfe_state* st, int32_t field, const double* in) {
     pfe_solver* S = st->s;
     CK(cudaSetDevice(S->device));
     const int d = S->d;
+    if (S->band_w) config_error("row-band solvers take their state from make_state only");
     if (field <= PFE_FIELD_BREGMAN) {
       double* dst = field == PFE_FIELD_Y ? st->y : (field == PFE_FIELD_P ? st->p : st->breg);
       upload_rows(S, in, S->n, d, dst, st->q);
@@ -1213,6 +1251,14 @@ int pfe_split_bregman(pfe_solver* s, pfe_state* st, int32_t max_iter, pfe_iterat
   return guarded([&] {
     CK(cudaSetDevice(s->device));
     if (max_iter <= 0) return;
+    if (s->band_w) {
+      if (cb || s->prm.conv_tol > 0.0) config_error("row-band solvers run fixed iteration counts without callbacks");
+      Team t{{st}, false};
+      s->ensure_log(max_iter);
+      team_split_bregman(t, max_iter);
+      team_check(t);
+      return;
+    }
     execute(st, kCallSplit, max_iter, 0, cb, user);
   });
 }
@@ -1221,6 +1267,12 @@ int pfe_run_soc(pfe_solver* s, pfe_state* st, int32_t soc_max, int32_t sb_max) {
   return guarded([&] {
     CK(cudaSetDevice(s->device));
     if (soc_max <= 0) return;
+    if (s->band_w) {
+      if (s->prm.conv_tol > 0.0) config_error("row-band solvers run fixed iteration counts (conv_tol = 0)");
+      Team t{{st}, false};
+      band_timed(s, [&] { team_run_soc(t, soc_max, std::max(0, sb_max)); });
+      return;
+    }
     execute(st, kCallSoc, soc_max, std::max(0, sb_max), nullptr, nullptr);
   });
 }
@@ -1228,6 +1280,19 @@ int pfe_run_soc(pfe_solver* s, pfe_state* st, int32_t soc_max, int32_t sb_max) {
 int pfe_two_stage(pfe_solver* s, pfe_state* st) {
   return guarded([&] {
     CK(cudaSetDevice(s->device));
+    if (s->band_w) {
+      if (s->prm.conv_tol > 0.0) config_error("row-band solvers run fixed iteration counts (conv_tol = 0)");
+      Team t{{st}, false};
+      band_timed(s, [&] {
+        team_run_soc(t, s->prm.soc_max, s->prm.sb_max_stage1);
+        if (s->prm.sb_max_stage2 > 0) {
+          s->ensure_log(s->prm.sb_max_stage2);
+          team_split_bregman(t, s->prm.sb_max_stage2);
+          team_check(t);
+        }
+      });
+      return;
+    }
     execute(st, kCallTwoStage, 0, 0, nullptr, nullptr);
   });
 }
@@ -1318,6 +1383,8 @@ int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_id
           if (acol[k] == r && aval[k] > 0.0) invd[r] = 1.0 / aval[k];  // pcg.cpp:15-20
     pfe_dev::Csr c{};
     c.n = n;
+    c.vb = 0;
+    c.ve = n;
     c.aptr = S->mem.upload(aptr, S->stream);
     c.acol = S->mem.upload(acol, S->stream);
     c.aval = S->mem.upload(aval, S->stream);
@@ -1401,6 +1468,68 @@ int pfe_shrink(int64_t count, const double* v, double gamma, const pfe_exec* x, 
     cudaFree(dv);
     cudaFree(dout);
     CK(e);
+  });
+}
+
+int pfe_band_plan(int32_t height, int32_t nranks, int32_t radius, int32_t rank, int32_t* out) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks || radius < 0) config_error("pfe_band_plan: bad arguments");
+    const BandPlan bp = band_plan(height, nranks, radius, rank);
+    out[0] = bp.r0;
+    out[1] = bp.r1;
+    out[2] = bp.lo;
+    out[3] = bp.hi;
+  });
+}
+
+int pfe_nccl_unique_id(uint8_t* out) {
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == PFE_NCCL_ID_BYTES, "NCCL unique id size");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int pfe_solver_create_band(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, const uint8_t* nccl_id,
+                           int32_t nranks, int32_t rank, pfe_solver** out) {
+  return guarded([&] {
+    require_device(x ? x->device : 0);
+    ncclComm_t comm = nullptr;
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      nccl_check(nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
+    }
+    try {
+      *out = create_band_solver(g, p, x, nranks, rank, comm);
+    } catch (...) {
+      if (comm) nccl().CommDestroy(comm);
+      throw;
+    }
+  });
+}
+
+int pfe_solve_banded(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t nbands, int32_t mode,
+                     const double* y0, double* y_out, pfe_report* rep) {
+  return guarded([&] {
+    std::vector<std::unique_ptr<pfe_solver>> solvers;
+    std::vector<std::unique_ptr<pfe_state>> states;
+    Team t;
+    t.emulated = true;
+    for (int b = 0; b < nbands; ++b) {
+      solvers.emplace_back(create_band_solver(g, p, x, nbands, b, nullptr));
+      states.emplace_back(create_band_state(solvers.back().get(), y0));
+      t.st.push_back(states.back().get());
+    }
+    team_run_soc(t, p->soc_max, p->sb_max_stage1);
+    if (mode == 1 && p->sb_max_stage2 > 0) {
+      for (auto& s : solvers) s->ensure_log(p->sb_max_stage2);
+      team_split_bregman(t, p->sb_max_stage2);
+      team_check(t);
+    }
+    team_gather_y(t, y_out);
+    if (rep && pfe_solver_report(solvers[0].get(), rep) != PFE_OK) throw Error(PFE_CUDA_ERROR, g_last_error);
   });
 }
 

@@ -64,14 +64,14 @@ struct TileIdx {
 template <int R, int D>
 __device__ __forceinline__ int num_tiles(const Grid<R>& g) {
   using G = TileGeo<R, D>;
-  return ((g.W + G::TW - 1) / G::TW) * ((g.H + G::TH - 1) / G::TH);
+  return ((g.W + G::TW - 1) / G::TW) * ((g.row_hi - g.row_lo + G::TH - 1) / G::TH);
 }
 template <int R, int D>
 __device__ __forceinline__ TileIdx tile_of(const Grid<R>& g, int t) {
   using G = TileGeo<R, D>;
   const int tiles_x = (g.W + G::TW - 1) / G::TW;
   const int ty = t / tiles_x;
-  return {ty * G::TH, (t - ty * tiles_x) * G::TW};
+  return {g.row_lo + ty * G::TH, (t - ty * tiles_x) * G::TW};
 }
 
 template <int R, int D>
@@ -130,7 +130,7 @@ __device__ __forceinline__ void stage_interior(const Grid<R>& g, TileIdx ti, con
     const int tv = c / PER, k = (c - tv * PER) * CH;
     const int ty = tv / G::TW, tx = tv - ty * G::TW;
     const int y = ti.y0 + ty, x = ti.x0 + tx;
-    const bool in = y < g.H && x < g.W;
+    const bool in = y < g.row_hi && x < g.W;
     cp_async(dst + tv * W + k, in ? src + (static_cast<long>(y) * g.W + x) * W + k : src, in, CH * 8);
   }
 }
@@ -147,14 +147,14 @@ __device__ __forceinline__ void for_tile_elements(const Grid<R>& g, TileIdx ti, 
       const int tv = e / D;
       const int ty = tv / G::TW, tx = tv - ty * G::TW;
       const int y = ti.y0 + ty, x = ti.x0 + tx;
-      if (y < g.H && x < g.W)
+      if (y < g.row_hi && x < g.W)
         f(tv, c, (ty + R) * G::HW + (tx + R), static_cast<long>(y) * g.W + x, 0);
     }
   } else {
     for (int tv = threadIdx.x; tv < G::NV; tv += G::NT) {
       const int ty = tv / G::TW, tx = tv - ty * G::TW;
       const int y = ti.y0 + ty, x = ti.x0 + tx;
-      if (y < g.H && x < g.W)
+      if (y < g.row_hi && x < g.W)
 #pragma unroll
         for (int c = 0; c < D; ++c) f(tv, c, (ty + R) * G::HW + (tx + R), static_cast<long>(y) * g.W + x, c);
     }
@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, S
         const double sh = shrink1(my + bo, a.gamma);
         const double bn = bo + (my - sh);
         acc += (fwd ? w : nw) * (sh - bn);
-        if (fwd) {
+        // the owner stores b (and s); in a row band, edges owned by the halo
+        // rows above are replicas that this band updates identically
+        if (fwd || static_cast<int>(v / g.W) - T::dy(s) < g.row_lo) {
           a.b_new[slot * D + c] = bn;
           if (a.s_out) a.s_out[slot * D + c] = sh;
         }

@@ -1,0 +1,153 @@
+"""Host-side logic of the multi-GPU row-band path, on CPU with torch.distributed
+(gloo, world_size 2): the band plan of the library (pfe_band_plan), the halo
+schedule (p' after SpMV, r after update, p' recomputed on the halo) and the
+rank-ordered reduction of gathered per-band totals, replayed in numpy.  The
+banded Jacobi-PCG must equal the single-domain one to rounding."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1612_06496_b200 import api
+from paper_1612_06496_b200.inputs import grid_graph, voronoi_image
+
+
+def test_band_plan_partitions_rows():
+    for H, P, R in [(321, 4, 1), (1024, 8, 2), (17, 2, 1), (10, 3, 2)]:
+        owned = []
+        for p in range(P):
+            r0, r1, lo, hi = api.band_plan(H, P, R, p)
+            owned.append((r0, r1))
+            assert lo == (max(0, r0 - R) if p > 0 else r0)
+            assert hi == (min(H, r1 + R) if p < P - 1 else r1)
+            assert r1 - r0 >= H // P
+        assert owned[0][0] == 0 and owned[-1][1] == H
+        assert all(owned[i][1] == owned[i + 1][0] for i in range(P - 1))
+
+
+def operator(g, lam=1.0, r=1.0):
+    """Dense-ish A = (lam/2) M^T M + (r/2) D as a scipy CSR (reference order irrelevant here)."""
+    import scipy.sparse as sp
+
+    hl = 0.5 * lam
+    a = sp.coo_matrix((np.r_[-hl * g.w * g.w, -hl * g.w * g.w], (np.r_[g.ei, g.ej], np.r_[g.ej, g.ei])),
+                      shape=(g.n, g.n)).tocsr()
+    diag = np.zeros(g.n)
+    np.add.at(diag, g.ei, hl * g.w * g.w)
+    np.add.at(diag, g.ej, hl * g.w * g.w)
+    diag += 0.5 * r * g.degree
+    return (a + sp.diags(diag)).tocsr(), diag
+
+
+def banded_pcg(rank, P, g, W, R, b_glob, x0_glob, iters, comm):
+    """Jacobi-PCG on band `rank` with the library's exchange schedule; fixed iterations."""
+    A, diag = operator(g)
+    r0, r1, lo, hi = api.band_plan(g.grid[0], P, R, rank)
+    own = slice((r0 - lo) * W, (r1 - lo) * W)  # owned rows in local indexing
+    loc = slice(lo * W, hi * W)
+    A_own = A[r0 * W:r1 * W, lo * W:hi * W]
+    invd = 1.0 / diag[loc]
+
+    def halo(vec):  # refresh the R halo rows of a local vector from the neighbours
+        if comm is None:
+            return
+        blk = R * W
+        reqs = []
+        import torch
+
+        t = torch.from_numpy(vec)
+        if rank > 0:
+            reqs.append(dist.isend(t[(r0 - lo) * W:(r0 - lo) * W + blk].clone(), rank - 1))
+            top = torch.empty(blk, dtype=torch.float64)
+            reqs.append(dist.irecv(top, rank - 1))
+        if rank < P - 1:
+            reqs.append(dist.isend(t[(r1 - lo) * W - blk:(r1 - lo) * W].clone(), rank + 1))
+            bot = torch.empty(blk, dtype=torch.float64)
+            reqs.append(dist.irecv(bot, rank + 1))
+        for q in reqs:
+            q.wait()
+        if rank > 0:
+            vec[:blk] = top.numpy()
+        if rank < P - 1:
+            vec[(r1 - lo) * W:] = bot.numpy()
+
+    def total(*vals):  # gather per-band totals, sum in rank order (identical on all bands)
+        import torch
+
+        mine = torch.tensor(vals, dtype=torch.float64)
+        if comm is None:
+            return list(mine.numpy())
+        allv = [torch.empty_like(mine) for _ in range(P)]
+        dist.all_gather(allv, mine)
+        s = np.zeros(len(vals))
+        for v in allv:
+            s = s + v.numpy()
+        return list(s)
+
+    x = x0_glob[loc].copy()
+    b = b_glob[loc]
+    r = np.zeros_like(x)
+    r[own] = b[own] - A_own @ x
+    p = np.zeros_like(x)
+    p[own] = invd[own] * r[own]
+    bb, rr, rz = total(b[own] @ b[own], r[own] @ r[own], r[own] @ p[own])
+    halo(p)
+    beta = 0.0
+    for k in range(1, iters + 1):
+        if k > 1:
+            p = invd * r + beta * p  # recomputed on owned + halo rows from exchanged r, p
+        q = A_own @ p
+        (pq,) = total(p[own] @ q)
+        halo(p)
+        alpha = rz / pq
+        x[own] = x[own] + alpha * p[own]
+        r[own] = r[own] - alpha * q
+        rr, rz_new = total(r[own] @ r[own], r[own] @ (invd[own] * r[own]))
+        halo(r)
+        beta = rz_new / rz
+        rz = rz_new
+    return x[own], (r0, r1)
+
+
+def _worker(rank, P, port, res_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    g, W, R, b, x0 = problem()
+    xs, (r0, r1) = banded_pcg(rank, P, g, W, R, b, x0, 12, True)
+    np.save(f"{res_path}_{rank}.npy", np.r_[r0, r1, xs])
+    dist.destroy_process_group()
+
+
+def problem():
+    rng = np.random.Generator(np.random.PCG64(3))
+    img, _ = voronoi_image(14, 11, 4, 0.05, rng)
+    g = grid_graph(img, 0.1, 1)
+    b = rng.normal(size=g.n)
+    x0 = rng.normal(size=g.n)
+    return g, 11, 1, b, x0
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_banded_pcg_two_ranks_gloo(tmp_path):
+    P = 2
+    res = str(tmp_path / "x")
+    mp.spawn(_worker, args=(P, free_port(), res), nprocs=P, join=True)
+    g, W, R, b, x0 = problem()
+    full, _ = banded_pcg(0, 1, g, W, R, b, x0, 12, None)
+    got = np.zeros(g.n)
+    for rank in range(P):
+        arr = np.load(f"{res}_{rank}.npy")
+        r0, r1 = int(arr[0]), int(arr[1])
+        got[r0 * W:r1 * W] = arr[2:]
+    assert np.abs(got - full).max() <= 1e-12 * np.abs(full).max()

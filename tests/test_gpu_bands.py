@@ -1,0 +1,67 @@
+"""Multi-GPU row-band decomposition, validated on one GPU:
+the library runs the exact banded algorithm with several bands emulated in
+one process (device copies instead of NCCL).  Bands must reproduce the
+single-domain solve up to the reduction order of the PCG scalars."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1612_06496_b200 import api
+from paper_1612_06496_b200.inputs import grid_graph, voronoi_image
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    s = np.sign(np.sum(a * b, axis=0))
+    s[s == 0] = 1
+    return np.linalg.norm(a * s - b) / np.linalg.norm(b)
+
+
+def image_graph(h, w, seed, radius):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    img, _ = voronoi_image(h, w, 6, 0.05, rng)
+    return grid_graph(img, 0.1, radius, 2.0 if radius == 2 else None)
+
+
+def params(d, soc=3, sb=5, stage2=0):
+    return api.PfeParams(dim=d, lambda_=1.0, r=1.0, soc_max=soc, sb_max_stage1=sb, sb_max_stage2=stage2,
+                         conv_tol=0.0, pcg=api.PcgConfig(1e-6, 50, api.Preconditioner.Jacobi))
+
+
+@pytest.mark.parametrize("radius,d,nbands", [(1, 4, 2), (1, 4, 3), (1, 8, 4), (2, 8, 2), (2, 3, 3), (1, 5, 2)])
+def test_bands_match_single_domain(radius, d, nbands):
+    g = image_graph(37, 53, 7 + nbands, radius)
+    prm = params(d)
+    y0 = api.random_embedding(g.n, d, 3, g.degree)
+    single = api.soc(g, prm, y0, persistent=False)
+    banded = api.soc_banded(g, prm, y0, nbands)
+    assert rel(banded, single) <= 1e-11
+    assert rel(banded, O.solve(g, prm, y0, mode=0)) <= 1e-10
+
+
+def test_bands_two_stage_and_bitwise_repeatable():
+    g = image_graph(40, 40, 11, 1)
+    prm = params(4, soc=2, sb=4, stage2=6)
+    y0 = api.random_embedding(g.n, 4, 8, g.degree)
+    a = api.soc_banded(g, prm, y0, 3, two_stage=True)
+    b = api.soc_banded(g, prm, y0, 3, two_stage=True)
+    assert np.array_equal(a, b)
+    assert rel(a, api.pfe_two_stage(g, prm, y0, persistent=False)) <= 1e-11
+
+
+def test_single_band_equals_unbanded_bitwise_elementwise_path():
+    """One band = the whole image: same kernels, same reductions except the
+    extra per-band total, so results agree to rounding."""
+    g = image_graph(30, 45, 2, 1)
+    prm = params(4)
+    y0 = api.random_embedding(g.n, 4, 1, g.degree)
+    assert rel(api.soc_banded(g, prm, y0, 1), api.soc(g, prm, y0, persistent=False)) <= 1e-13
+
+
+def test_band_rejects_non_grid_and_thin_bands():
+    g = image_graph(6, 20, 1, 2)
+    prm = params(2)
+    y0 = api.random_embedding(g.n, 2, 1, g.degree)
+    with pytest.raises(api.ConfigError, match="at least R image rows"):
+        api.soc_banded(g, prm, y0, 4)
