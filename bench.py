@@ -236,6 +236,67 @@ def cpu_baseline(cfg, y0):
                       f"{os.cpu_count()} host cores; oracle port (reference needs Eigen3, absent)"}
 
 
+def run_bands(args, rank, world, local):
+    """Strong scaling of ONE image split into row bands, one band per GPU (NCCL halos)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1612_06496_b200 import api
+    from paper_1612_06496_b200.inputs import make_config
+
+    cfg = make_config(args.config, seed=0)  # the same image on every rank
+    g, prm = cfg.graph, cfg.params
+    y0 = api.random_embedding(g.n, prm.dim, cfg.y0_seed, g.degree)
+    inner_per_step = prm.soc_max * prm.sb_max_stage1
+    obj = [api.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    torch.cuda.set_device(local)
+    solver = api.BandSolver(g, prm, obj[0], world, rank, device=local, warn=False)
+    st = solver.make_state(y0)
+    for _ in range(args.warmup):
+        st.reset()
+        solver.run_soc(st, prm.soc_max, prm.sb_max_stage1)
+    barrier(world)
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            st.reset()
+            barrier(world)
+            solver.run_soc(st, prm.soc_max, prm.sb_max_stage1)
+            times.append(solver.last_ms() * 1e-3)
+    t_max = allreduce_max(sum(times), world)
+    # end to end: state from host y0, solve, gathered Y back on the host
+    e2e = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        s2 = solver.make_state(y0)
+        solver.run_soc(s2, prm.soc_max, prm.sb_max_stage1)
+        _ = s2.y
+        e2e.append(time.perf_counter() - t0)
+        s2.close()
+    e2e_max = allreduce_max(sum(e2e), world)
+    if rank != 0:
+        return None
+    rep = solver.report()
+    return {
+        "metric": METRIC, "value": args.steps * inner_per_step / t_max, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Voronoi RGB image)",
+        "config": {"workload": cfg.name, "description": cfg.description, "n": g.n, "m": g.m, "d": prm.dim,
+                   "parallelism": f"{world} row bands (NCCL halo exchange + gathered PCG totals)",
+                   "l2": "inputs larger than L2" if g.n * prm.dim * 8 > 126e6 else "resident",
+                   "topology": ["csr", "grid8", "grid24"][rep["topology"]]},
+        "roofline": None,
+        "cpu_baseline": None,
+        "e2e": {"value": args.steps * inner_per_step / e2e_max, "unit": UNIT,
+                "h2d_bytes_per_step": g.n * prm.dim * 8, "d2h_bytes_per_step": g.n * prm.dim * 8,
+                "call": "BandSolver.make_state(y0) + run_soc + gathered state.y"},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+    }
+
+
 def run_gpu(args, rank, world, local):
     import ctypes as C
 
@@ -407,10 +468,14 @@ def main():
                     "persistent cooperative kernel (grid graphs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--bands", action="store_true", help="N>1: split one image of a grid config into row "
+                    "bands, one per GPU (strong scaling) instead of independent replicas")
     args = ap.parse_args()
     rank, world, local = dist_init(args.gpus)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
+    elif args.bands and world > 1:
+        line = run_bands(args, rank, world, local)
     else:
         line = run_gpu(args, rank, world, local)
     if rank == 0 and line is not None:
