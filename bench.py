@@ -364,11 +364,12 @@ def run_gpu(args, rank, world, local):
         kt = s.kernel_times()
         its, _, _ = s.pcg_log()
         k_inner = its[before:].max(axis=1)
+        kind = s.report()["persistent_kind"]
         s.close()
-        return kt, k_inner
+        return kt, k_inner, kind
 
     # multi-kernel path: per-kernel split (also the path k-NN graphs use)
-    kt_m, _ = instrumented(False)
+    kt_m, _, _ = instrumented(False)
     share = {k: v[0] for k, v in kt_m.items()}
     tot_ms = sum(share.values()) or 1.0
     per_kernel = {}
@@ -383,19 +384,35 @@ def run_gpu(args, rank, world, local):
     if persistent_used:
         # the persistent kernel runs whole split_bregman calls: its algorithmic
         # bytes are those of every phase it executes
-        kt_p, k_inner = instrumented(True)
-        ms, cnt = kt_p["sb_persistent"]
         bi = algorithmic_bytes("pcg_init", g.n, g.m, prm.dim)
         bs = algorithmic_bytes("pcg_spmv", g.n, g.m, prm.dim)
         bu = algorithmic_bytes("pcg_update", g.n, g.m, prm.dim)
         bsb = algorithmic_bytes("sb_pass", g.n, g.m, prm.dim)
-        total_b = float(sum(bi + int(k) * (bs + bu) + bsb for k in k_inner))
-        gbs = total_b / (ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_sb_persistent", "achieved": gbs, "peak": peak, "unit": "GB/s",
-                    "frac": gbs / peak, "traffic": ncu_traffic(cfg.name, "k_sb_persistent"),
+
+        def persistent_roofline(mode):
+            kt_p, k_inner, kind = instrumented(mode)
+            ms, cnt = kt_p["sb_persistent"]
+            total_b = float(sum(bi + int(k) * (bs + bu) + bsb for k in k_inner))
+            return kind, ms, cnt, total_b, total_b / (ms * 1e-3) / 1e9
+
+        kind, ms, cnt, total_b, gbs = persistent_roofline(True)
+        kname = {1: "k_sb_persistent", 2: "k_sb_resident"}.get(kind, "k_sb_persistent")
+        tiled = None
+        if kind == 2:  # the streaming (tiled) persistent kernel on the same workload, for comparison
+            _, ms_t, cnt_t, tb_t, gbs_t = persistent_roofline("tiled")
+            tiled = {"kernel": "k_sb_persistent", "avg_launch_us": 1e3 * ms_t / cnt_t, "GB/s": gbs_t,
+                     "frac": gbs_t / peak}
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": gbs, "peak": peak, "unit": "GB/s",
+                    "frac": gbs / peak, "traffic": ncu_traffic(cfg.name, kname),
                     "peak_source": peak_src, "alg_bytes_per_launch": total_b / cnt,
                     "avg_launch_us": 1e3 * ms / cnt, "launches": cnt,
+                    "model": ("compulsory bytes of the streamed algorithm (every PCG / split-Bregman phase "
+                              "reads and writes its operands once, DESIGN.md §4) / kernel time"
+                              + ("; k_sb_resident keeps the PCG state in shared memory, so its real HBM "
+                                 "traffic is far below this and frac > 1 is possible: it is bounded by grid "
+                                 "barrier latency, see profiles/" if kind == 2 else "")),
                     "timing": "CUDA events around every launch of one instrumented step after the timed region",
+                    "tiled_persistent": tiled,
                     "kernels_multi_kernel_path": per_kernel}
     else:
         dom = max(("pcg_spmv", "pcg_update", "sb_pass"), key=lambda k: share[k])

@@ -91,7 +91,10 @@ typedef struct pfe_exec {
   int32_t profile;      /* 1: time every kernel launch with CUDA events */
   int32_t persistent;   /* 1: pixel-grid graphs run each split_bregman call as
                            one persistent cooperative kernel (grid barriers,
-                           device-side PCG control); 0: one kernel per phase */
+                           device-side PCG control), keeping the PCG state in
+                           shared memory when it fits; 2: the same kernel
+                           without the shared-memory-resident variant;
+                           0: one kernel per phase */
 } pfe_exec;
 
 /* Run report (PcgReport aggregation, pcg.hpp:21-26). */
@@ -106,7 +109,8 @@ typedef struct pfe_report {
   int64_t n;
   int64_t m;
   int32_t d;
-  int32_t pad;
+  int32_t persistent_kind;       /* kernel of the last persistent launch: 0 none,
+                                    1 tiled (streams HBM/L2), 2 shared-memory resident */
   double setup_seconds;          /* host + device setup of pfe_solver_create */
 } pfe_report;
 

@@ -37,7 +37,7 @@ class pfe_report(C.Structure):
     _fields_ = [("inner_iterations", C.c_int64), ("pcg_iterations", C.c_int64),
                 ("pcg_column_iterations", C.c_int64), ("nonconverged", C.c_int64), ("failed", C.c_int64),
                 ("jacobi_fallback", C.c_int32), ("topology", C.c_int32), ("n", C.c_int64), ("m", C.c_int64),
-                ("d", C.c_int32), ("pad", C.c_int32), ("setup_seconds", C.c_double)]
+                ("d", C.c_int32), ("persistent_kind", C.c_int32), ("setup_seconds", C.c_double)]
 
 
 KERNEL_CLASSES = ("pcg_init", "pcg_spmv", "pcg_update", "pcg_finalize", "sb_pass", "rhs", "projection",

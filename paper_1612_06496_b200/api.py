@@ -146,8 +146,10 @@ def degree_vector(ei, ej, w, n) -> np.ndarray:
 
 
 def _exec(device=0, use_graphs=True, warn=True, profile=False, persistent=True) -> N.pfe_exec:
-    return N.pfe_exec(int(device), int(bool(use_graphs)), int(bool(warn)), int(bool(profile)),
-                      int(bool(persistent)))
+    # persistent: True (shared-memory-resident kernel when the state fits),
+    # "tiled" (persistent kernel streaming tiles from HBM/L2), False (one kernel per phase)
+    mode = 2 if persistent == "tiled" else (persistent if type(persistent) is int else int(bool(persistent)))
+    return N.pfe_exec(int(device), int(bool(use_graphs)), int(bool(warn)), int(bool(profile)), mode)
 
 
 def _colmajor(a, rows=None, cols=None) -> np.ndarray:
@@ -265,7 +267,7 @@ class PfeSolver:
     def report(self) -> dict:
         r = N.pfe_report()
         _check(N.load().pfe_solver_report(self._h, C.byref(r)))
-        return {k: getattr(r, k) for k, _ in N.pfe_report._fields_ if k != "pad"}
+        return {k: getattr(r, k) for k, _ in N.pfe_report._fields_}
 
     def pcg_log(self):
         d = self.params.dim
@@ -322,7 +324,8 @@ def pfe_two_stage(g: WeightedGraph, params: PfeParams, y0, **kw) -> np.ndarray:
 
 
 def split_bregman(g: WeightedGraph, d_vec, p, b, params: PfeParams, y_init, max_iter: int,
-                  on_iterate: Optional[Callable[[int, np.ndarray], None]] = None, device: int = 0) -> np.ndarray:
+                  on_iterate: Optional[Callable[[int, np.ndarray], None]] = None, device: int = 0,
+                  persistent=True) -> np.ndarray:
     """Standalone split_bregman with M = difference_matrix(g) (solver.cpp:138-182)."""
     y_init = np.asarray(y_init, dtype=np.float64)
     if y_init.ndim == 1:
@@ -331,7 +334,7 @@ def split_bregman(g: WeightedGraph, d_vec, p, b, params: PfeParams, y_init, max_
     gg = WeightedGraph(g.n, g.ei, g.ej, g.w, np.asarray(d_vec, dtype=np.float64), grid=g.grid)
     gc = gg.to_c()
     pc = params.to_c()
-    xc = _exec(device, True, False)
+    xc = _exec(device, True, False, persistent=persistent)
     pa, ba, ya = _colmajor(p, n, d), _colmajor(b, n, d), _colmajor(y_init, n, d)
     out = np.empty(n * d)
     cb = N.ITERATE_FN()

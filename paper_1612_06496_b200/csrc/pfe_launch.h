@@ -50,6 +50,8 @@ struct PersistIn {
   double* part_b;
   unsigned long long* trace;  // optional phase trace (null: off)
   int trace_cap;
+  int allow_resident;  // run the shared-memory-resident kernel when the state fits
+  double* part_c;      // its init partials (2 x 3 x kMaxD x #SMs)
 };
 
 struct LaunchTable {
@@ -73,8 +75,9 @@ struct LaunchTable {
   // Largest resident grid (blocks) of the heaviest kernels, for partial sizing.
   int (*max_blocks_per_sm)();
   // Persistent cooperative split-Bregman kernel (grid topologies only).
-  // Returns false when the topology has no persistent kernel.
-  bool (*sb_persistent)(const TopoDesc&, const PersistIn&, Launch);
+  // Returns the variant launched: 0 none (topology without one), 1 tiled,
+  // 2 shared-memory resident.
+  int (*sb_persistent)(const TopoDesc&, const PersistIn&, Launch);
   // block partials -> nq * D totals (nq = 1 or 3), one block
   void (*local_totals)(int nq, const double* part, int nb, double* out, cudaStream_t);
 };

@@ -1,6 +1,7 @@
 // Template bodies of the launch table (included by pfe_kernels_d*.cu only).
 #pragma once
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -9,6 +10,7 @@
 #include "pfe_polar.cuh"
 #include "pfe_stencil.cuh"
 #include "pfe_persist.cuh"
+#include "pfe_resident.cuh"
 
 namespace pfe_host {
 
@@ -142,8 +144,53 @@ struct Impl {
                             double* rq, double hr, Launch l) {
     k_project_apply<D><<<l.grid, kBlock, 0, l.stream>>>(n, y, sqd, breg, w, p, rq, hr); PFE_LAUNCHED(__func__);
   }
+  // Region grid of the shared-memory-resident kernel: rgx x rgy <= #SMs
+  // regions minimising the largest region + ring (the per-block work), under
+  // the shared-memory, per-thread element and ring limits.  ok = false: the
+  // state does not fit; the tiled persistent kernel runs instead.
+  struct ResPlan {
+    bool ok = false;
+    int gx = 0, gy = 0, hw = 0, np = 0;
+    size_t smem = 0;
+  };
   template <int R>
-  static bool persist_grid(const Grid<R>& g, const PersistIn& in, Launch l) {
+  static ResPlan res_plan(const Grid<R>& g, int sms) {
+    using G = ResGeo<D, R>;
+    static size_t avail = 0;
+    if (avail == 0) {
+      int dev = 0, optin = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, k_sb_resident<D, R>);
+      avail = static_cast<size_t>(optin) - fa.sharedSizeBytes;
+      cudaFuncSetAttribute(k_sb_resident<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)avail);
+    }
+    ResPlan best;
+    if (g.row_lo != 0 || g.row_hi != g.H) return best;  // single-domain solvers only
+    const int max_blocks = std::min(sms, G::kMaxBlocks);
+    for (int gy = 1; gy <= g.H && gy <= max_blocks; ++gy) {
+      const int gx = std::min(g.W, max_blocks / gy);
+      const int rh = (g.H + gy - 1) / gy, rw = (g.W + gx - 1) / gx;
+      const int hw = rw + 2 * R, np = hw * (rh + 2 * R);
+      const size_t smem = sizeof(double) * static_cast<size_t>(np) * G::kPerPos;
+      const long ring = 2L * R * hw + 2L * R * rh;
+      if (smem > avail || static_cast<long>(rh) * rw * D > static_cast<long>(G::NT) * G::EPT ||
+          ring * D > static_cast<long>(G::NT) * G::HR)
+        continue;
+      if (!best.ok || np < best.np || (np == best.np && gx * gy < best.gx * best.gy)) {
+        best.ok = true;
+        best.gx = gx;
+        best.gy = gy;
+        best.hw = hw;
+        best.np = np;
+        best.smem = smem;
+      }
+    }
+    return best;
+  }
+  template <int R>
+  static int persist_grid(const Grid<R>& g, const PersistIn& in, Launch l) {
     constexpr size_t smem = sizeof(double) * PersistGeo<D, R>::kSmem;
     static int per_sm = -1;
     if (per_sm < 0) {
@@ -181,18 +228,34 @@ struct Impl {
     a.part_b = in.part_b;
     a.trace = in.trace;
     a.trace_cap = in.trace_cap;
+    a.part_c = in.part_c;
     void* args[] = {&a};
+    if (in.allow_resident) {
+      const ResPlan rp = res_plan<R>(g, l.sm);
+      if (rp.ok) {
+        a.rgx = rp.gx;
+        a.rgy = rp.gy;
+        a.rhw = rp.hw;
+        a.rnp = rp.np;
+        const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_sb_resident<D, R>),
+                                                          dim3(rp.gx * rp.gy), dim3(ResGeo<D, R>::NT), args,
+                                                          rp.smem, l.stream);
+        if (e != cudaSuccess)
+          throw std::runtime_error(std::string("cooperative launch failed: ") + cudaGetErrorString(e));
+        return 2;
+      }
+    }
     const int grid = per_sm * l.sm;
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_sb_persistent<D, R>),
                                                       dim3(grid), dim3(TileGeo<R, D>::NT), args, smem, l.stream);
     if (e != cudaSuccess)
       throw std::runtime_error(std::string("cooperative launch failed: ") + cudaGetErrorString(e));
-    return true;
+    return 1;
   }
-  static bool sb_persistent(const TopoDesc& t, const PersistIn& in, Launch l) {
+  static int sb_persistent(const TopoDesc& t, const PersistIn& in, Launch l) {
     if (t.kind == kTopoGrid1) return persist_grid<1>(t.g1, in, l);
     if (t.kind == kTopoGrid2) return persist_grid<2>(t.g2, in, l);
-    return false;
+    return 0;
   }
   static void local_totals(int nq, const double* part, int nb, double* out, cudaStream_t s) {
     if (nq == 3)

@@ -63,6 +63,10 @@ struct PersistArgs {
   int trace_cap;
   double* part_b;    // SpMV block partials: alternating buffers so a fast block never
                      // overwrites partials a slow block is still reducing
+  // shared-memory-resident variant (pfe_resident.cuh) only
+  double* part_c;    // init partials, two buffers alternating by inner iteration
+  int rgx, rgy;      // region grid: blocks = rgx * rgy, block b owns region (b / rgx, b % rgx)
+  int rhw, rnp;      // smem pitch (max region width + 2R) and positions per plane
 };
 
 // Per-block column state (identical in every block).
@@ -293,8 +297,8 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
             if (e < total) {
               xv[u] = xs[e];
               rv[u] = a.r[e];
-              pv[u] = __ldg(pin + e);
-              qv[u] = __ldg(a.q + e);
+              pv[u] = __ldcg(pin + e);  // written earlier in this kernel: L2-coherent loads
+              qv[u] = __ldcg(a.q + e);
               iv[u] = __ldg(g.invd + e / D);
             }
           }
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
               if constexpr (G::kStageB)
                 bo = Bo[(s * G::NO + opos) * D + c];
               else
-                bo = __ldg(b_old + slot * D + c);
+                bo = __ldcg(b_old + slot * D + c);
             }
             const double nw = -w;
             const double my = w * P[opos * D + c] + nw * P[jpos * D + c];

@@ -72,21 +72,40 @@ void require_device(int dev) {
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
     config_error("no CUDA device available: the B200 PFE solver has no CPU fallback");
   if (dev < 0 || dev >= count) config_error("CUDA device ordinal out of range");
-  cudaDeviceProp prop{};
-  CK(cudaGetDeviceProperties(&prop, dev));
-  if (prop.major < 10)
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major < 10) {
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, dev));
     config_error(std::string("device ") + prop.name + " is not sm_100-class; this library is built for sm_100a only");
+  }
   CK(cudaSetDevice(dev));
 }
 
-// Owner of a set of device allocations.
+// Owner of a set of device allocations.  Allocations are stream-ordered
+// (cudaMallocAsync / cudaFreeAsync on the owner's stream) from the device's
+// default memory pool, which keeps freed memory (release threshold: never),
+// so creating and destroying solvers and states in a loop -- the one-call
+// C ABI does that on every call -- re-uses device memory instead of paying
+// cudaMalloc / cudaFree each time.
+void retain_pool_memory(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = ~static_cast<uint64_t>(0);
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[dev] = true;
+}
+
 struct DevPool {
   std::vector<void*> ptrs;
+  cudaStream_t stream = nullptr;  // set before the first allocation
   template <class T>
   T* alloc(size_t count) {
     if (count == 0) count = 1;
     void* p = nullptr;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    CK(cudaMallocAsync(&p, count * sizeof(T), stream));
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -99,13 +118,15 @@ struct DevPool {
   void release(void* p) {
     auto it = std::find(ptrs.begin(), ptrs.end(), p);
     if (it != ptrs.end()) {
-      cudaFree(p);
+      cudaFreeAsync(p, stream);
       ptrs.erase(it);
     }
   }
-  ~DevPool() {
-    for (void* p : ptrs) cudaFree(p);
+  void free_all() {
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
+    ptrs.clear();
   }
+  ~DevPool() { free_all(); }
 };
 
 // Per-kernel-class CUDA-event timing (pfe_exec.profile).
@@ -191,6 +212,8 @@ struct pfe_solver {
   int sm = 148;
   bool use_graphs = true, warn = true;
   bool persistent = true;  // grid topologies: one cooperative launch per split_bregman call
+  bool resident = true;    // ... with the PCG state resident in shared memory when it fits
+  int persist_kind = 0;    // variant of the last persistent launch (pfe_report::persistent_kind)
   int row_lo = 0, row_hi = -1;  // owned rows of a row-band solver (-1: every row)
   // Row-band (multi-GPU) solver: this solver owns global image rows
   // [band_r0, band_r1) of a band_h x band_w grid and stores local rows
@@ -219,6 +242,7 @@ struct pfe_solver {
   Ctl* h_ctl = nullptr;  // pinned mirror
   double* partials = nullptr;    // init / update partials (and objective, norms)
   double* partials_b = nullptr;  // spmv partials
+  double* partials_c = nullptr;  // init partials of the resident persistent kernel (two sets)
   int max_grid = 0;
   double* rbuf = nullptr;
   int qr_blocks = 1;
@@ -237,6 +261,7 @@ struct pfe_solver {
   double last_ms = 0.0;  // device time of the last split_bregman / run_soc / two_stage call
 
   ~pfe_solver() {
+    mem.free_all();  // stream-ordered frees need the stream
     if (comm && g_comm_destroy) g_comm_destroy(comm);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -531,18 +556,22 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   S->warn = x ? x->warn != 0 : true;
   S->prof.on = x ? x->profile != 0 : false;
   S->persistent = x ? x->persistent != 0 : true;
-  if (const char* tr = std::getenv("PFE_TRACE"); tr && tr[0] == '1') {
-    S->trace = S->mem.alloc<unsigned long long>(kTraceCap);
-    CK(cudaMemset(S->trace, 0, sizeof(unsigned long long) * kTraceCap));
-  }
+  S->resident = x ? x->persistent == 1 : true;
+  retain_pool_memory(S->device);
   CK(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&S->aux, cudaStreamNonBlocking));
+  S->mem.stream = S->stream;
+  if (const char* tr = std::getenv("PFE_TRACE"); tr && tr[0] == '1') {
+    S->trace = S->mem.alloc<unsigned long long>(kTraceCap);
+    CK(cudaMemsetAsync(S->trace, 0, sizeof(unsigned long long) * kTraceCap, S->stream));
+  }
   CK(cudaDeviceGetAttribute(&S->sm, cudaDevAttrMultiProcessorCount, S->device));
   S->d = d;
   S->tab = &pfe_host::table_for(d);
   S->max_grid = S->sm * std::max(8, S->tab->max_blocks_per_sm());
   S->partials = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * 3 * pfe_dev::kMaxD);
   S->partials_b = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * pfe_dev::kMaxD);
+  S->partials_c = S->mem.alloc<double>(static_cast<size_t>(S->sm) * 6 * pfe_dev::kMaxD);
   S->ctl = S->mem.alloc<Ctl>(1);
   CK(cudaMemsetAsync(S->ctl, 0, sizeof(Ctl), S->stream));
   CK(cudaMallocHost(&S->h_ctl, sizeof(Ctl)));
@@ -638,6 +667,7 @@ void state_init_from_y0(pfe_state* st) {
 pfe_state* create_state(pfe_solver* S, const double* y0_host) {
   auto st = std::make_unique<pfe_state>();
   st->s = S;
+  st->mem.stream = S->stream;
   const size_t nd = static_cast<size_t>(S->n) * S->d;
   const size_t ed = static_cast<size_t>(S->edge_rows) * S->d;
   st->y = st->ybuf[0] = st->mem.alloc<double>(nd);
@@ -884,8 +914,10 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
       in.part_b = S->partials_b;
       in.trace = S->trace;
       in.trace_cap = S->trace ? kTraceCap : 0;
+      in.allow_resident = S->resident && S->nranks == 1 ? 1 : 0;
+      in.part_c = S->partials_c;
       S->prof.begin(7, S->stream);
-      S->tab->sb_persistent(S->topo, in, S->lv());
+      S->persist_kind = S->tab->sb_persistent(S->topo, in, S->lv());
       S->prof.end(S->stream);
       for (int k = 0; k < nrun; ++k) {
         std::swap(st->y, st->y2);
@@ -1107,6 +1139,7 @@ int pfe_solver_report(const pfe_solver* s, pfe_report* out) {
     r.m = s->m;
     r.d = s->d;
     r.jacobi_fallback = s->jacobi_fallback ? 1 : 0;
+    r.persistent_kind = s->persist_kind;
     r.setup_seconds = s->setup_s;
     const long cnt = std::min(s->inner_launched, s->log_cap);
     std::vector<int> it(static_cast<size_t>(cnt) * s->d), stt(static_cast<size_t>(cnt) * s->d);
@@ -1310,14 +1343,33 @@ int pfe_state_objective(pfe_solver* s, pfe_state* st, double* out) {
 int pfe_solve(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t mode, const double* y0,
               double* y_out, pfe_report* rep) {
   return guarded([&] {
+    // PFE_E2E_TIMING=1: wall time of each stage on stderr
+    static const bool timing = [] {
+      const char* e = std::getenv("PFE_E2E_TIMING");
+      return e && e[0] == '1';
+    }();
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
     std::unique_ptr<pfe_solver> S(create_solver(g, p, x));
+    auto t1 = now();
     std::unique_ptr<pfe_state> st(create_state(S.get(), y0));
+    auto t2 = now();
     if (mode == 1)
       execute(st.get(), kCallTwoStage, 0, 0, nullptr, nullptr);
     else
       execute(st.get(), kCallSoc, p->soc_max, p->sb_max_stage1, nullptr, nullptr);
+    auto t3 = now();
     download_rows(S.get(), st->y, S->n, S->d, y_out, st->q);
     if (rep && pfe_solver_report(S.get(), rep) != PFE_OK) throw Error(PFE_CUDA_ERROR, g_last_error);
+    auto t4 = now();
+    st.reset();
+    S.reset();
+    auto t5 = now();
+    if (timing) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "pfe_solve: create %.2f state %.2f solve %.2f download+report %.2f destroy %.2f ms\n",
+                   ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
+    }
   });
 }
 

@@ -14,7 +14,9 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-PHASES = {1: "init", 3: "spmv", 5: "update", 6: "finalize", 8: "sb_pass"}
+PHASES = {1: "init", 3: "spmv", 5: "update", 6: "finalize", 8: "sb_pass",
+          # fine-grained points of the resident kernel (end of each sub-step)
+          10: "beta_red", 11: "p_dir", 12: "q_Ap", 13: "x_r_upd", 14: "alpha_red"}
 
 
 def main():

@@ -175,26 +175,63 @@ def test_graph_and_host_driven_agree_bitwise():
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("radius,d", [(1, 4), (1, 8), (1, 3), (2, 8)])
-def test_persistent_kernel_matches_multi_kernel_path(radius, d):
-    """The cooperative persistent split-Bregman kernel computes the same
+@pytest.mark.parametrize("kind", ["resident", "tiled"])
+@pytest.mark.parametrize("radius,d", [(1, 4), (1, 8), (1, 3), (2, 8), (2, 2)])
+def test_persistent_kernel_matches_multi_kernel_path(radius, d, kind):
+    """The cooperative persistent split-Bregman kernels (state resident in
+    shared memory, or tiles streamed from L2/HBM) compute the same
     per-element arithmetic as the one-kernel-per-phase path; only the
     reduction trees (grid sizes) differ."""
     g = small_image(48, 70, seed=5, radius=radius, sigma_xy=2.0 if radius == 2 else None)
     prm = jacobi(d, soc=3, sb=6)
     y0 = api.random_embedding(g.n, d, 4, g.degree)
-    a = api.soc(g, prm, y0, persistent=True)
+    mode = True if kind == "resident" else "tiled"
+    s = api.PfeSolver(g, prm, warn=False, persistent=mode)
+    st = s.make_state(y0)
+    s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
+    a = st.y
+    assert s.report()["persistent_kind"] == (2 if kind == "resident" else 1)
     b = api.soc(g, prm, y0, persistent=False)
     assert rel_fro_signed(a, b) <= 1e-12
     exp = O.solve(g, prm, y0, mode=0)
     assert rel_fro_signed(a, exp) <= 1e-10
     # state after a persistent call is complete (split_s materialised)
-    s = api.PfeSolver(g, prm, warn=False)
+    s = api.PfeSolver(g, prm, warn=False, persistent=mode)
     st = s.make_state(y0)
     s.run_soc(st, 2, 4)
     full = O.solve(g, jacobi(d, soc=2, sb=4), y0, mode=0, full_state=True)
     assert np.abs(st.split_s - full["split_s"]).max() <= 1e-9
     assert np.abs(st.split_b - full["split_b"]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("h,w,radius,d", [(1, 200, 1, 4), (300, 4, 1, 4), (5, 300, 2, 4), (17, 6, 2, 2),
+                                            (150, 151, 1, 4), (3, 4, 1, 1)])
+def test_resident_kernel_region_shapes(h, w, radius, d):
+    """Region grids with 1-pixel-wide regions, regions thinner than the ring,
+    images smaller than the region count: same result as the multi-kernel path."""
+    g = small_image(h, w, seed=h + w, radius=radius, sigma_xy=2.0 if radius == 2 else None)
+    prm = jacobi(d, soc=2, sb=4)
+    y0 = api.random_embedding(g.n, d, 6, g.degree)
+    s = api.PfeSolver(g, prm, warn=False)
+    st = s.make_state(y0)
+    s.run_soc(st, 2, 4)
+    assert s.report()["persistent_kind"] == 2
+    b = api.soc(g, prm, y0, persistent=False)
+    assert rel_fro_signed(st.y, b) <= 1e-12
+
+
+def test_resident_kernel_with_callback_and_conv_tol():
+    """One launch per inner iteration (callback / relative-change test): the
+    rhs handed from launch to launch keeps the iteration identical."""
+    g = small_image(60, 80, seed=9)
+    prm = jacobi(4, soc=2, sb=5)
+    y0 = api.random_embedding(g.n, 4, 3, g.degree)
+    p, b0 = y0, 0.1 * y0
+    seen = []
+    a = api.split_bregman(g, g.degree, p, b0, prm, y0 * 0.5, 5, on_iterate=lambda it, y: seen.append(it))
+    b = api.split_bregman(g, g.degree, p, b0, prm, y0 * 0.5, 5, persistent=False)
+    assert seen == list(range(5))
+    assert rel_fro_signed(a, b) <= 1e-12
 
 
 def test_deterministic_runs():
