@@ -175,7 +175,7 @@ struct Impl {
       const int hw = rw + 2 * R, np = hw * (rh + 2 * R);
       const size_t smem = sizeof(double) * static_cast<size_t>(np) * G::kPerPos;
       const long ring = 2L * R * hw + 2L * R * rh;
-      if (smem > avail || static_cast<long>(rh) * rw * D > static_cast<long>(G::NT) * G::EPT ||
+      if (smem > avail || static_cast<long>(rh) * rw * G::U > static_cast<long>(G::NT) * G::EPT ||
           ring * D > static_cast<long>(G::NT) * G::HR)
         continue;
       if (!best.ok || np < best.np || (np == best.np && gx * gy < best.gx * best.gy)) {

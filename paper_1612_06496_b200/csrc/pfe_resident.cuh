@@ -37,6 +37,7 @@ struct ResGeo {
   static constexpr int HR = 2;     // ring elements per thread, max
   static constexpr int kMaxBlocks = 256;  // reduce_partials_warp limit
   static constexpr int S = GridTopo<R>::S;
+  static constexpr int U = D;                     // units (pixel, column) per pixel
   static constexpr int kPerPos = 3 * D + S + 2;  // shared doubles per ring/interior position
   static constexpr bool kFix = (32 % D == 0);
   static constexpr int V = kFix ? 1 : D;

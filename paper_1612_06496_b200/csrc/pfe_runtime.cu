@@ -416,11 +416,32 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   if (grid) {
     slot_of.resize(static_cast<size_t>(m));
     const int S_ = grad == 1 ? 4 : 12;
+    // j - i identifies (dy, dx) uniquely since |dx| <= R < W / 2; the column
+    // of i (tracked incrementally: edges are sorted by i) rules out wrap-around
+    int cur_i = -1, xi = 0;
     for (long k = 0; k < m && grid; ++k) {
-      if (k > 0 && !(g.ei[k - 1] < g.ei[k] || (g.ei[k - 1] == g.ei[k] && g.ej[k - 1] < g.ej[k]))) grid = false;
-      const int s = grid_slot(grad, gw, g.ei[k], g.ej[k]);
+      const int i = g.ei[k], j = g.ej[k];
+      if (k > 0 && !(g.ei[k - 1] < i || (g.ei[k - 1] == i && g.ej[k - 1] < j))) grid = false;
+      if (i != cur_i) {
+        xi = i % gw;
+        cur_i = i;
+      }
+      const long dlt = static_cast<long>(j) - i;
+      const int dy = static_cast<int>((dlt + grad) / gw);
+      const int dx = static_cast<int>(dlt - static_cast<long>(dy) * gw);
+      int s = -1;
+      if (xi + dx >= 0 && xi + dx < gw) {
+        if (grad == 1) {
+          if (dy == 0 && dx == 1) s = 0;
+          else if (dy == 1 && dx >= -1 && dx <= 1) s = 2 + dx;
+        } else {
+          if (dy == 0 && (dx == 1 || dx == 2)) s = dx - 1;
+          else if (dy == 1 && dx >= -2 && dx <= 2) s = 4 + dx;
+          else if (dy == 2 && dx >= -2 && dx <= 2) s = 9 + dx;
+        }
+      }
       if (s < 0) grid = false;
-      slot_of[k] = static_cast<long>(g.ei[k]) * S_ + s;
+      slot_of[k] = static_cast<long>(i) * S_ + s;
     }
   }
   if (grid) {
@@ -434,27 +455,27 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     // diag(A)_v: incident edges in edge-index order = backward slots (u
     // ascending) then forward slots; absent slots hold 0 and add +0.0.
     std::vector<double> diag(n, 0.0);
-    std::vector<int> off(S_);
+    int off[12], sdy[12], sdx[12];
     for (int s = 0; s < S_; ++s) {
-      const int dy = grad == 1 ? (s == 0 ? 0 : 1) : (s < 2 ? 0 : (s < 7 ? 1 : 2));
-      const int dx = grad == 1 ? (s == 0 ? 1 : s - 2) : (s < 2 ? s + 1 : (s < 7 ? s - 4 : s - 9));
-      off[s] = dy * gw + dx;
+      sdy[s] = grad == 1 ? (s == 0 ? 0 : 1) : (s < 2 ? 0 : (s < 7 ? 1 : 2));
+      sdx[s] = grad == 1 ? (s == 0 ? 1 : s - 2) : (s < 2 ? s + 1 : (s < 7 ? s - 4 : s - 9));
+      off[s] = sdy[s] * gw + sdx[s];
     }
-    for (int v = 0; v < n; ++v) {
-      const int y = v / gw, x = v % gw;
-      double acc = 0.0;
-      for (int s = S_ - 1; s >= 0; --s) {
-        const int dy = off[s] >= gw - grad ? (off[s] + grad) / gw : 0, dx = off[s] - dy * gw;
-        const int yy = y - dy, xx = x - dx;
-        if (yy < 0 || xx < 0 || xx >= gw) continue;
-        const double w = wf[static_cast<size_t>(v - off[s]) * S_ + s];
-        acc += (hl * w) * w;
+    for (int y = 0, v = 0; y < gh; ++y) {
+      for (int x = 0; x < gw; ++x, ++v) {
+        double acc = 0.0;
+        for (int s = S_ - 1; s >= 0; --s) {
+          const int yy = y - sdy[s], xx = x - sdx[s];
+          if (yy < 0 || xx < 0 || xx >= gw) continue;
+          const double w = wf[static_cast<size_t>(v - off[s]) * S_ + s];
+          acc += (hl * w) * w;
+        }
+        for (int s = 0; s < S_; ++s) {
+          const double w = wf[static_cast<size_t>(v) * S_ + s];
+          acc += (hl * w) * w;
+        }
+        diag[v] = acc;
       }
-      for (int s = 0; s < S_; ++s) {
-        const double w = wf[static_cast<size_t>(v) * S_ + s];
-        acc += (hl * w) * w;
-      }
-      diag[v] = acc;
     }
     finish_diag(diag);
     double* dwf = S->mem.upload(wf, st);
