@@ -100,7 +100,10 @@ void retain_pool_memory(int dev) {
 
 struct DevPool {
   std::vector<void*> ptrs;
-  cudaStream_t stream = nullptr;  // set before the first allocation
+  cudaStream_t stream = nullptr;   // allocation stream, set before the first allocation
+  cudaStream_t fstream = nullptr;  // free stream: a state may outlive its solver's
+                                   // stream, so states free on the legacy stream (every
+                                   // call synchronizes before returning: nothing pending)
   template <class T>
   T* alloc(size_t count) {
     if (count == 0) count = 1;
@@ -118,12 +121,12 @@ struct DevPool {
   void release(void* p) {
     auto it = std::find(ptrs.begin(), ptrs.end(), p);
     if (it != ptrs.end()) {
-      cudaFreeAsync(p, stream);
+      cudaFreeAsync(p, fstream);
       ptrs.erase(it);
     }
   }
   void free_all() {
-    for (void* p : ptrs) cudaFreeAsync(p, stream);
+    for (void* p : ptrs) cudaFreeAsync(p, fstream);
     ptrs.clear();
   }
   ~DevPool() { free_all(); }
@@ -581,7 +584,7 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   retain_pool_memory(S->device);
   CK(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&S->aux, cudaStreamNonBlocking));
-  S->mem.stream = S->stream;
+  S->mem.stream = S->mem.fstream = S->stream;
   if (const char* tr = std::getenv("PFE_TRACE"); tr && tr[0] == '1') {
     S->trace = S->mem.alloc<unsigned long long>(kTraceCap);
     CK(cudaMemsetAsync(S->trace, 0, sizeof(unsigned long long) * kTraceCap, S->stream));

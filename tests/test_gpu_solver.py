@@ -234,6 +234,26 @@ def test_resident_kernel_with_callback_and_conv_tol():
     assert rel_fro_signed(a, b) <= 1e-12
 
 
+def test_state_outliving_its_solver_is_safe():
+    """Destroying a solver before its state (Python GC order) must not break
+    later solvers: states return their memory to the pool independently."""
+    g = small_image(30, 40, seed=4)
+    prm = jacobi(4, soc=2, sb=3)
+    y0 = api.random_embedding(g.n, 4, 2, g.degree)
+    s = api.PfeSolver(g, prm, warn=False)
+    st = s.make_state(y0)
+    s.run_soc(st, 2, 3)
+    s.close()
+    del st
+    for _ in range(3):
+        s2 = api.PfeSolver(g, prm, warn=False)
+        st2 = s2.make_state(y0)
+        s2.run_soc(st2, 2, 3)
+        y = st2.y
+        s2.close()
+    assert rel_fro_signed(y, api.soc(g, prm, y0, persistent=False)) <= 1e-12
+
+
 def test_deterministic_runs():
     # test_solver.cpp:353-365
     rng = np.random.Generator(np.random.PCG64(41))
