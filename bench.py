@@ -177,6 +177,15 @@ def algorithmic_bytes(kind, n, m, d):
 
 
 # ------------------------------------------------------------------ arms ---
+def sample_inner(cfg, core_seconds):
+    """Inner iterations of the oracle that fit in ~core_seconds of single-core
+    work: C2's 20 inner iterations take ~1.8 s, and the cost scales with the
+    (m + n) d of the graph."""
+    d = cfg.params.dim
+    est = 0.09 * (cfg.graph.m * d + cfg.graph.n * d) / (613454 * 4 + 154401 * 4)
+    return int(max(1, min(cfg.params.sb_max_stage1, core_seconds // max(est, 1e-9))))
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
@@ -193,6 +202,7 @@ def run_reference(args, rank, world):
     O.set_threads(threads)
     sample = api.PfeParams(**{**prm.__dict__})
     sample.soc_max = 1
+    sample.sb_max_stage1 = sample_inner(cfg, 10.0 * threads)  # <= ~10 s per step on `threads` cores
     inner = sample.sb_max_stage1
     for _ in range(args.warmup if args.warmup < 1 else 1):
         O.solve(g, sample, y0, mode=0)
@@ -227,13 +237,15 @@ def cpu_baseline(cfg, y0):
     O.set_threads(1)
     sample = api.PfeParams(**{**cfg.params.__dict__})
     sample.soc_max = 1
+    sample.sb_max_stage1 = sample_inner(cfg, 15.0)
     t0 = time.perf_counter()
     O.solve(cfg.graph, sample, y0, mode=0)
     dt = time.perf_counter() - t0
     inner = sample.sb_max_stage1
     return {"value": inner / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"first outer iteration ({inner} inner iterations, {dt:.1f} s) of {cfg.name} on 1 of "
-                      f"{os.cpu_count()} host cores; oracle port (reference needs Eigen3, absent)"}
+            "sample": f"first outer iteration truncated to {inner} inner iterations ({dt:.1f} s incl. operator "
+                      f"set-up and one projection) of {cfg.name} on 1 of {os.cpu_count()} host cores; oracle "
+                      f"port (reference needs Eigen3, absent)"}
 
 
 def run_bands(args, rank, world, local):

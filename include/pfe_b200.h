@@ -240,6 +240,18 @@ int pfe_random_embedding(int32_t n, int32_t d, uint64_t seed, const double* degr
 int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
                int32_t* labels);
 
+/* k-NN graph builder for point sets (configs C1 / C5).  No reference
+ * counterpart: the reference has no k-NN builder; this
+ * is the harness definition of paper_1612_06496_b200/inputs.py knn_graph --
+ * exact k nearest neighbours (ascending distance, then index) on the GPU,
+ * sigma = median directed k-NN distance, union-symmetrised edges (i < j,
+ * lexicographic), w = exp(-|x_i - x_j|^2 / (2 sigma^2)) dropped below 1e-12,
+ * degree summed in edge order (graph.cpp:15-22).  points: row-major n x dim
+ * (dim <= 32); k <= 32; ei / ej / w need capacity n * k, degree n.  Writes the
+ * edge count to *m_out and sigma to *sigma_out. */
+int pfe_knn_graph(int32_t n, int32_t dim, const double* points, int32_t k, int32_t device, int32_t* ei, int32_t* ej,
+                  double* w, double* degree, int64_t* m_out, double* sigma_out);
+
 #ifdef __cplusplus
 }
 #endif

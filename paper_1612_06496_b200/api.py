@@ -475,6 +475,23 @@ def kmeans(points, k: int, seed: int, max_iter: int = 100) -> np.ndarray:
     return lab
 
 
+def knn_graph_gpu(points, k: int, device: int = 0) -> "WeightedGraph":
+    """Union-symmetrised k-NN heat-kernel graph built on the GPU (pfe_knn_graph);
+    same definition as inputs.knn_graph (the host builder)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    if pts.ndim == 1:
+        pts = pts.reshape(-1, 1)
+    n, dim = pts.shape
+    cap = n * int(k)
+    ei, ej = np.empty(cap, np.int32), np.empty(cap, np.int32)
+    w, deg = np.empty(cap), np.empty(n)
+    m, sigma = C.c_int64(), C.c_double()
+    _check(N.load().pfe_knn_graph(n, dim, N.dptr(pts), int(k), int(device), N.iptr(ei), N.iptr(ej), N.dptr(w),
+                                  N.dptr(deg), C.byref(m), C.byref(sigma)))
+    mm = m.value
+    return WeightedGraph(n, ei[:mm].copy(), ej[:mm].copy(), w[:mm].copy(), deg, sigma.value)
+
+
 # ------------------------------------------------------------ row bands ----
 def band_plan(height: int, nranks: int, radius: int, rank: int) -> Tuple[int, int, int, int]:
     """Rows owned (r0, r1) and stored (lo, hi) by band `rank` (host only)."""

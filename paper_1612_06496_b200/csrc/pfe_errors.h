@@ -16,5 +16,8 @@ struct Error : std::runtime_error {
 void random_embedding(int n, int d, uint64_t seed, const double* deg, double* out);
 void d_orthonormalize(int n, int d, const double* a, const double* deg, double* out);
 void kmeans(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
+void knn_search(int n, int dim, const double* pts, int k, double* d2, int32_t* idx);
+long knn_graph_from_lists(int n, int k, const double* d2, const int32_t* idx, int32_t* ei, int32_t* ej, double* w,
+                          double* degree, double* sigma_out);
 
 }  // namespace pfe_host

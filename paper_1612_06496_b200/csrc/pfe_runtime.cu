@@ -1645,6 +1645,19 @@ int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t s
   return guarded([&] { pfe_host::kmeans(n, d, points, k, seed, max_iter, labels); });
 }
 
+int pfe_knn_graph(int32_t n, int32_t dim, const double* points, int32_t k, int32_t device, int32_t* ei, int32_t* ej,
+                  double* w, double* degree, int64_t* m_out, double* sigma_out) {
+  return guarded([&] {
+    if (!points || !ei || !ej || !w || !degree || !m_out || !sigma_out) config_error("knn_graph: null argument");
+    require_device(device);
+    const size_t nk = static_cast<size_t>(n) * std::max(k, 0);
+    std::vector<double> d2(nk);
+    std::vector<int32_t> idx(nk);
+    pfe_host::knn_search(n, dim, points, k, d2.data(), idx.data());
+    *m_out = pfe_host::knn_graph_from_lists(n, k, d2.data(), idx.data(), ei, ej, w, degree, sigma_out);
+  });
+}
+
 }  // extern "C"
 
 namespace pfe_host {

@@ -90,12 +90,17 @@ def grid_graph(rgb: np.ndarray, sigma_rgb: float, radius: int = 1, sigma_xy: Opt
     return WeightedGraph(n, ei.astype(np.int32), ej.astype(np.int32), ew, deg, sigma_rgb, grid=(h, wd, radius))
 
 
-def knn_graph(points: np.ndarray, k: int) -> WeightedGraph:
+def knn_graph(points: np.ndarray, k: int, gpu: bool = False) -> WeightedGraph:
     """Union-symmetrised k-NN graph, heat kernel with sigma = median directed k-NN distance.
 
     w_ij = exp(-|x_i - x_j|^2 / (2 sigma^2)) once per unordered pair (not summed).
-    Brute force (host); intended for the small C1 configuration and tests.
+    Brute force on the host (the small C1 configuration and tests), or on the
+    GPU with ``gpu=True`` (pfe_knn_graph; C5).
     """
+    if gpu:
+        from .api import knn_graph_gpu
+
+        return knn_graph_gpu(points, k)
     n = points.shape[0]
     sq = (points ** 2).sum(1)
     nbr = np.empty((n, k), dtype=np.int64)
@@ -207,7 +212,7 @@ def make_config(name: str, seed: int = 0, scale: Optional[Tuple[int, int]] = Non
         wts /= wts.sum()
         comp = rng.choice(32, size=n, p=wts)
         pts = means[comp] + rng.normal(size=(n, 16)) * stds[comp, None]
-        g = knn_graph(pts, 16)
+        g = knn_graph(pts, 16, gpu=True)  # 10^6 points: built once on the GPU (timed separately)
         return Config("c5", g, _params(16, 10, 20, 1e-6), 32, seed, comp,
                       f"{n} points in R^16, 32-component GMM, sym. 16-NN, d=16, 10x20")
     raise ValueError(f"unknown config {name}")
