@@ -215,6 +215,15 @@ struct Grid {
       }
     }
   }
+  // same interface as Csr::visitA_b / visitE_b (stencil rows need no batching)
+  template <int B, class L, class F>
+  __device__ __forceinline__ void visitA_b(int v, L&& load, F&& use) const {
+    visitA(v, [&](int u, double av) { use(av, load(u)); });
+  }
+  template <int B, class L, class F>
+  __device__ __forceinline__ void visitE_b(int v, L&& load, F&& use) const {
+    visitE(v, [&](int u, double w, long slot, bool fwd) { use(u, w, slot, fwd, load(u, slot)); });
+  }
 };
 
 // General graph (k-NN, arbitrary edge lists): explicit CSR of A (diagonal in
@@ -227,8 +236,8 @@ struct Csr {
   const int* __restrict__ acol;
   const double* __restrict__ aval;
   const int* __restrict__ iptr;
-  const int* __restrict__ inbr;
-  const int* __restrict__ ieid;
+  const int* __restrict__ inbr;  // incidence: neighbour (device row)
+  const int* __restrict__ ieid;  // edge id << 1 | [this vertex is the edge's first endpoint]
   const double* __restrict__ iw;
   const double* __restrict__ invd;
   int vb, ve;  // owned vertex range
@@ -245,8 +254,57 @@ struct Csr {
   __device__ __forceinline__ void visitE(int v, F&& f) const {
     const int b = __ldg(iptr + v), e = __ldg(iptr + v + 1);
     for (int k = b; k < e; ++k) {
-      const int u = __ldg(inbr + k);
-      f(u, __ldg(iw + k), static_cast<long>(__ldg(ieid + k)), u > v);
+      const int code = __ldg(ieid + k);  // edge id << 1 | [v is the first endpoint]
+      f(__ldg(inbr + k), __ldg(iw + k), static_cast<long>(code >> 1), (code & 1) != 0);
+    }
+  }
+  // Batched visits for gather-bound k-NN rows: the index loads of a batch of
+  // B entries, then their B gathers load(...), are all issued before
+  // use(...) consumes them in row / edge order (the summation order is
+  // unchanged; only the memory round trips overlap).
+  template <int B, class L, class F>
+  __device__ __forceinline__ void visitA_b(int v, L&& load, F&& use) const {
+    const int b = __ldg(aptr + v), e = __ldg(aptr + v + 1);
+    for (int k0 = b; k0 < e; k0 += B) {
+      using G = decltype(load(0));
+      int cu[B];
+      double av[B];
+      G g[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const bool ok = k0 + j < e;
+        cu[j] = ok ? __ldg(acol + k0 + j) : -1;
+        av[j] = ok ? __ldg(aval + k0 + j) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) g[j] = load(cu[j]);
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) use(av[j], g[j]);
+    }
+  }
+  template <int B, class L, class F>
+  __device__ __forceinline__ void visitE_b(int v, L&& load, F&& use) const {
+    const int b = __ldg(iptr + v), e = __ldg(iptr + v + 1);
+    for (int k0 = b; k0 < e; k0 += B) {
+      using G = decltype(load(0, 0L));
+      int cu[B], cc[B];
+      double cw[B];
+      G g[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const bool ok = k0 + j < e;
+        cu[j] = ok ? __ldg(inbr + k0 + j) : -1;
+        cc[j] = ok ? __ldg(ieid + k0 + j) : 0;
+        cw[j] = ok ? __ldg(iw + k0 + j) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) g[j] = load(cu[j], static_cast<long>(cc[j] >> 1));
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) use(cu[j], cw[j], static_cast<long>(cc[j] >> 1), (cc[j] & 1) != 0, g[j]);
     }
   }
 };

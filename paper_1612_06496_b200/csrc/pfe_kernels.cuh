@@ -225,7 +225,7 @@ __device__ __forceinline__ bool update_prologue(const PcgArgs& a, ColView<D>& cv
 
 // ---------------------------------------------------------------- PCG init --
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_pcg_init(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   double acc[3][V] = {};
   const long total = static_cast<long>(topo.vend()) * TPV;
@@ -234,11 +234,12 @@ __global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double ax[V] = {};
-    topo.visitA(v, [&](int u, double av) {
-      const Row<V> xu = ldg_row<V>(a.x0 + static_cast<long>(u) * D + c0);
+    topo.template visitA_b<8>(
+        v, [&](int u) { return ldg_row<V>(a.x0 + static_cast<long>(u) * D + c0); },
+        [&](double av, const Row<V>& xu) {
 #pragma unroll
-      for (int k = 0; k < V; ++k) ax[k] += av * xu.a[k];
-    });
+          for (int k = 0; k < V; ++k) ax[k] += av * xu.a[k];
+        });
     const Row<V> b = ld_row<V>(a.rhs + static_cast<long>(v) * D + c0);
     const double id = topo.inv_diag(v);
     Row<V> r, z;
@@ -256,9 +257,40 @@ __global__ void __launch_bounds__(kBlock) k_pcg_init(Topo topo, PcgArgs a) {
   block_reduce_store<3, D, V>(acc, a.part_a);
 }
 
+// ----------------------------------------------- PCG direction (CSR rows) --
+// [stop test, beta] p' = D^-1 r + beta p_old for every vertex (pcg.cpp:86-88),
+// ahead of k_pcg_spmv on general graphs: their SpMV then gathers p' once per
+// neighbour instead of re-forming it from r and p_old.  The SpMV repeats the
+// same prologue (same partials, same decisions; its writes are idempotent).
+template <int D, class Topo>
+__global__ void __launch_bounds__(kBlock) k_pcg_pdir(Topo topo, PcgArgs a) {
+  constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
+  __shared__ ColView<D> cv;
+  if (!spmv_prologue<D, kBlock>(a, cv)) return;
+  const int gfirst = (static_cast<int>(threadIdx.x) % TPV) * V;
+  double beta[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) beta[k] = cv.coef[gfirst + k];
+  double* pnew = pcg_pnew(a);
+  const double* pold = pcg_pold(a);
+  const long total = static_cast<long>(topo.vend()) * TPV;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int v = static_cast<int>(e / TPV);
+    const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
+    const Row<V> rv = ldg_row<V>(a.r + static_cast<long>(v) * D + c0);
+    const Row<V> po = ldg_row<V>(pold + static_cast<long>(v) * D + c0);
+    const double id = topo.inv_diag(v);
+    Row<V> pu;
+#pragma unroll
+    for (int k = 0; k < V; ++k) pu.a[k] = id * rv.a[k] + beta[k] * po.a[k];
+    st_row<V>(pnew + static_cast<long>(v) * D + c0, pu);
+  }
+}
+
 // ------------------------------------------------------- PCG SpMV (+ p update)
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_pcg_spmv(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   __shared__ ColView<D> cv;
   if (!spmv_prologue<D, kBlock>(a, cv)) return;
@@ -277,13 +309,16 @@ __global__ void __launch_bounds__(kBlock) k_pcg_spmv(Topo topo, PcgArgs a) {
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double q[V] = {};
     Row<V> pv;
-    if (first) {
+    if (first || !Topo::kGrid) {
+      // CSR rows: p' was formed for every vertex by k_pcg_pdir (one gather per
+      // neighbour instead of three); first iteration: p = z from the init
       pv = ldg_row<V>(pnew + static_cast<long>(v) * D + c0);
-      topo.visitA(v, [&](int u, double av) {
-        const Row<V> pu = ldg_row<V>(pnew + static_cast<long>(u) * D + c0);
+      topo.template visitA_b<8>(
+          v, [&](int u) { return ldg_row<V>(pnew + static_cast<long>(u) * D + c0); },
+          [&](double av, const Row<V>& pu) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) q[k] += av * pu.a[k];
-      });
+            for (int k = 0; k < V; ++k) q[k] += av * pu.a[k];
+          });
     } else {
       // p_u = z_u + beta p_u with z_u = D^-1_u r_u, recomputed identically
       // for every row that reads vertex u (pcg.cpp:86-88).
@@ -442,7 +477,7 @@ struct SbArgs {
 // right-hand side (solver.cpp:83-84) is accumulated from the same edge values:
 // rhs_v = hl * sum_e M_ev (s_e - b_e') + rq_v.
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock) k_sb_pass(Topo topo, SbArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_sb_pass(Topo topo, SbArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
@@ -454,15 +489,23 @@ __global__ void __launch_bounds__(kBlock) k_sb_pass(Topo topo, SbArgs a) {
 #pragma unroll
     for (int k = 0; k < V; ++k) bad |= !isfinite(yv.a[k]);
     double acc[V] = {};
-    topo.visitE(v, [&](int u, double w, long slot, bool fwd) {
-      const Row<V> yu = ldg_row<V>(a.y + static_cast<long>(u) * D + c0);
-      Row<V> bo;
+    struct YB {
+      Row<V> y, b;
+    };
+    auto load = [&](int u, long slot) {
+      YB g;
+      g.y = ldg_row<V>(a.y + static_cast<long>(u) * D + c0);
       if (a.b_old) {
-        bo = ldg_row<V>(a.b_old + slot * D + c0);
+        g.b = ldg_row<V>(a.b_old + slot * D + c0);
       } else {
 #pragma unroll
-        for (int k = 0; k < V; ++k) bo.a[k] = 0.0;
+        for (int k = 0; k < V; ++k) g.b.a[k] = 0.0;
       }
+      return g;
+    };
+    topo.template visitE_b<4>(v, load, [&](int, double w, long slot, bool fwd, const YB& g) {
+      const Row<V>& yu = g.y;
+      const Row<V>& bo = g.b;
       Row<V> bn, sv;
       const double nw = -w;
 #pragma unroll

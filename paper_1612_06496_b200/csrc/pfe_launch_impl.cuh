@@ -99,6 +99,9 @@ struct Impl {
   static void pcg_spmv(const TopoDesc& t, const PcgArgs& a, Launch l) {
     if (t.kind == kTopoGrid1) return grid_spmv<1>(t.g1, a, l);
     if (t.kind == kTopoGrid2) return grid_spmv<2>(t.g2, a, l);
+    if (a.phase != 0) {
+      k_pcg_pdir<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+    }
     k_pcg_spmv<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void pcg_update(const TopoDesc& t, const PcgArgs& a, Launch l) {

@@ -238,6 +238,11 @@ struct pfe_solver {
   int d = 0;
   TopoDesc topo;
   std::vector<long> edge_row;  // edge e -> row of the device edge arrays
+  // General graphs store vertices in a locality order (BFS): perm_h[v] = the
+  // device row of vertex v (empty / null: identity).  Only storage moves; every
+  // row keeps its terms in the reference's order.
+  std::vector<int> perm_h;
+  int* perm_d = nullptr;
   long edge_rows = 0;
   DevPool mem;
   double *deg = nullptr, *sqd = nullptr, *diag = nullptr, *invd = nullptr;
@@ -523,7 +528,39 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     for (int k = iptr[v]; k < iptr[v + 1]; ++k) acc += (hl * iw[k]) * iw[k];
     diag[v] = acc;
   }
-  finish_diag(diag);
+  // storage order: BFS over the incidence graph (components in vertex order),
+  // so the rows a vertex gathers sit near its own and stay in L2 / L1
+  std::vector<int> perm(n, -1), inv(n);
+  {
+    int next = 0, head = 0;
+    std::vector<int> queue(n);
+    for (int s0 = 0; s0 < n; ++s0) {
+      if (perm[s0] >= 0) continue;
+      perm[s0] = next;
+      queue[next++] = s0;
+      while (head < next) {
+        const int v = queue[head++];
+        for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
+          const int u = inbr[k];
+          if (perm[u] < 0) {
+            perm[u] = next;
+            queue[next++] = u;
+          }
+        }
+      }
+    }
+    for (int v = 0; v < n; ++v) inv[perm[v]] = v;
+  }
+  {
+    // diag / inv_diag in storage order ((r/2) d_v is added last, as finish_diag does)
+    std::vector<double> dperm(n), invd(n);
+    for (int v = 0; v < n; ++v) dperm[perm[v]] = diag[v] + dterm * g.deg[v];
+    for (int x = 0; x < n; ++x)
+      invd[x] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (dperm[x] > 0.0 ? 1.0 / dperm[x] : 1.0);
+    for (int v = 0; v < n; ++v) diag[v] = dperm[perm[v]];
+    S->diag = S->mem.upload(dperm, st);
+    S->invd = S->mem.upload(invd, st);
+  }
 
   // General CSR: A rows sorted by column with duplicate columns summed in
   // edge order (stable sort), exact zeros dropped, diagonal in place.
@@ -532,7 +569,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   acol.reserve(static_cast<size_t>(2 * m + n));
   aval.reserve(static_cast<size_t>(2 * m + n));
   std::vector<std::pair<int, double>> row;
-  for (int v = 0; v < n; ++v) {
+  for (int x = 0; x < n; ++x) {
+    const int v = inv[x];  // storage row x holds vertex v's row, in the reference's column order
     row.clear();
     for (int k = iptr[v]; k < iptr[v + 1]; ++k) row.emplace_back(inbr[k], -((hl * iw[k]) * iw[k]));
     row.emplace_back(v, diag[v]);
@@ -548,14 +586,37 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
         for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
       }
       if (s != 0.0) {
-        acol.push_back(col);
+        acol.push_back(perm[col]);
         aval.push_back(s);
       }
     }
-    aptr[v + 1] = static_cast<int>(acol.size());
+    aptr[x + 1] = static_cast<int>(acol.size());
   }
-  S->edge_row.resize(static_cast<size_t>(m));
-  std::iota(S->edge_row.begin(), S->edge_row.end(), 0L);
+  // edge storage follows the vertex storage order: the edges a vertex owns
+  // (it is their first endpoint) are consecutive rows of the edge arrays
+  std::vector<int> epos(static_cast<size_t>(m));
+  for (int x = 0, next = 0; x < n; ++x) {
+    const int v = inv[x];
+    for (int k = iptr[v]; k < iptr[v + 1]; ++k)
+      if (inbr[k] > v) epos[ieid[k]] = next++;
+  }
+  // incidence lists in storage order: (neighbour row, w, edge row << 1 | [v is
+  // the edge's first endpoint]), each in increasing edge index
+  std::vector<int> iptr2(static_cast<size_t>(n) + 1, 0), inbr2(static_cast<size_t>(2 * m)),
+      ieid2(static_cast<size_t>(2 * m));
+  std::vector<double> iw2(static_cast<size_t>(2 * m));
+  for (int x = 0, at = 0; x < n; ++x) {
+    const int v = inv[x];
+    for (int k = iptr[v]; k < iptr[v + 1]; ++k, ++at) {
+      inbr2[at] = perm[inbr[k]];
+      ieid2[at] = (epos[ieid[k]] << 1) | (inbr[k] > v ? 1 : 0);
+      iw2[at] = iw[k];
+    }
+    iptr2[x + 1] = at;
+  }
+  S->perm_h = perm;
+  S->perm_d = S->mem.upload(perm, st);
+  S->edge_row.assign(epos.begin(), epos.end());
   S->edge_rows = m;
   pfe_dev::Csr c{};
   c.n = n;
@@ -564,10 +625,10 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   c.aptr = S->mem.upload(aptr, st);
   c.acol = S->mem.upload(acol, st);
   c.aval = S->mem.upload(aval, st);
-  c.iptr = S->mem.upload(iptr, st);
-  c.inbr = S->mem.upload(inbr, st);
-  c.ieid = S->mem.upload(ieid, st);
-  c.iw = S->mem.upload(iw, st);
+  c.iptr = S->mem.upload(iptr2, st);
+  c.inbr = S->mem.upload(inbr2, st);
+  c.ieid = S->mem.upload(ieid2, st);
+  c.iw = S->mem.upload(iw2, st);
   c.invd = S->invd;
   S->topo.kind = pfe_host::kTopoCsr;
   S->topo.csr = c;
@@ -604,6 +665,19 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   std::memset(S->h_ctl, 0, sizeof(Ctl));
 }
 
+// deg and sqrt(deg) in device row order (after build_topology chose it).
+void upload_degree(pfe_solver* S, const double* degree) {
+  const int n = S->n;
+  std::vector<double> deg(n), sqd(n);
+  for (int v = 0; v < n; ++v) {
+    const int x = S->perm_h.empty() ? v : S->perm_h[v];
+    deg[x] = degree[v];
+    sqd[x] = std::sqrt(degree[v]);
+  }
+  S->deg = S->mem.upload(deg, S->stream);
+  S->sqd = S->mem.upload(sqd, S->stream);
+}
+
 // TSQR grid: about 8 tiles of rows per block, at most max_grid blocks.
 int qr_blocks_for(const pfe_solver* S, long n) {
   const long rows_per_block = 8L * (pfe_dev::kQrRows - S->d);
@@ -622,11 +696,8 @@ pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exe
   init_common(S.get(), x, p->dim);
   S->n = g->n;
   S->m = g->m;
-  std::vector<double> deg(g->degree, g->degree + g->n), sqd(g->n);
-  for (int v = 0; v < g->n; ++v) sqd[v] = std::sqrt(deg[v]);
-  S->deg = S->mem.upload(deg, S->stream);
-  S->sqd = S->mem.upload(sqd, S->stream);
   build_topology(S.get(), hg, g->grid_h, g->grid_w, g->grid_radius);
+  upload_degree(S.get(), g->degree);
   S->qr_blocks = qr_blocks_for(S.get(), g->n);
   S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * S->d * S->d);
   S->wmat = S->mem.alloc<double>(static_cast<size_t>(S->d) * S->d);
@@ -638,20 +709,23 @@ pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exe
 
 // ------------------------------------------------------------- state ------
 
-__global__ void k_colmajor_to_rows(long n, int d, const double* __restrict__ src, double* dst) {
+// Column-major host layout <-> device rows (perm: vertex -> device row, or null).
+__global__ void k_colmajor_to_rows(long n, int d, const double* __restrict__ src, double* dst,
+                                   const int* __restrict__ perm) {
   const long total = n * d, stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const long v = e / d;
     const int j = static_cast<int>(e - v * d);
-    dst[e] = src[v + j * n];
+    dst[(perm ? perm[v] : v) * d + j] = src[v + j * n];
   }
 }
-__global__ void k_rows_to_colmajor(long n, int d, const double* __restrict__ src, double* dst) {
+__global__ void k_rows_to_colmajor(long n, int d, const double* __restrict__ src, double* dst,
+                                   const int* __restrict__ perm) {
   const long total = n * d, stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const long v = e % n;
     const int j = static_cast<int>(e / n);
-    dst[e] = src[v * d + j];
+    dst[e] = src[(perm ? perm[v] : v) * d + j];
   }
 }
 __global__ void k_scale_rows(long n, int d, const double* __restrict__ s, const double* __restrict__ y, double* out) {
@@ -663,11 +737,13 @@ __global__ void k_scale_rows(long n, int d, const double* __restrict__ s, const 
 // host col-major n x d -> device row-major via a staging buffer
 void upload_rows(pfe_solver* S, const double* host, long n, int d, double* dst, double* staging) {
   CK(cudaMemcpyAsync(staging, host, sizeof(double) * n * d, cudaMemcpyHostToDevice, S->stream));
-  k_colmajor_to_rows<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, staging, dst);
+  k_colmajor_to_rows<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, staging, dst,
+                                                                             n == S->n ? S->perm_d : nullptr);
   CK(cudaGetLastError());
 }
 void download_rows(pfe_solver* S, const double* src, long n, int d, double* host, double* staging) {
-  k_rows_to_colmajor<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, src, staging);
+  k_rows_to_colmajor<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, src, staging,
+                                                                             n == S->n ? S->perm_d : nullptr);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(host, staging, sizeof(double) * n * d, cudaMemcpyDeviceToHost, S->stream));
   CK(cudaStreamSynchronize(S->stream));
@@ -1414,11 +1490,8 @@ int pfe_split_bregman_standalone(const pfe_graph* g, const double* p, const doub
     S->warn = false;
     S->n = g->n;
     S->m = g->m;
-    std::vector<double> deg(g->degree, g->degree + g->n), sqd(g->n);
-    for (int v = 0; v < g->n; ++v) sqd[v] = std::sqrt(deg[v]);
-    S->deg = S->mem.upload(deg, S->stream);
-    S->sqd = S->mem.upload(sqd, S->stream);
     build_topology(S.get(), hg, g->grid_h, g->grid_w, g->grid_radius);
+    upload_degree(S.get(), g->degree);
     S->qr_blocks = 1;
     S->rbuf = S->mem.alloc<double>(static_cast<size_t>(d) * d);
     S->wmat = S->mem.alloc<double>(static_cast<size_t>(d) * d);
