@@ -296,7 +296,7 @@ def run_bands(args, rank, world, local):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Voronoi RGB image)",
         "config": {"workload": cfg.name, "description": cfg.description, "n": g.n, "m": g.m, "d": prm.dim,
-                   "parallelism": f"{world} row bands (NCCL halo exchange + gathered PCG totals)",
+                   "parallelism": (f"{world} row bands (NCCL halo exchange + gathered PCG totals)" if g.grid else f"{world} vertex ranges (NCCL ghost-row exchange + gathered PCG totals)"),
                    "l2": "inputs larger than L2" if g.n * prm.dim * 8 > 126e6 else "resident",
                    "topology": ["csr", "grid8", "grid24"][rep["topology"]]},
         "roofline": None,

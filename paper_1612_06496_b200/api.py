@@ -502,9 +502,9 @@ def band_plan(height: int, nranks: int, radius: int, rank: int) -> Tuple[int, in
 
 def soc_banded(g: WeightedGraph, params: PfeParams, y0, nbands: int, two_stage: bool = False,
                device: int = 0) -> np.ndarray:
-    """The multi-GPU row-band algorithm with `nbands` bands emulated on one device."""
-    if not g.grid:
-        raise ConfigError("row bands need a pixel-grid graph (grid hint)")
+    """The multi-GPU partitioned algorithm with `nbands` parts emulated on one
+    device: row bands for pixel grids (grid hint), vertex ranges with ghost
+    rows for general graphs."""
     y0c = _colmajor(y0, g.n, params.dim)
     out = np.empty(g.n * params.dim)
     gc, pc, xc = g.to_c(), params.to_c(), _exec(device, False, False, persistent=False)
@@ -521,7 +521,8 @@ def nccl_unique_id() -> bytes:
 
 
 class BandSolver(PfeSolver):
-    """One row band of a multi-GPU solve (one process per GPU, NCCL between bands).
+    """One row band (pixel grids) or vertex range (general graphs) of a
+    multi-GPU solve (one process per GPU, NCCL between ranks).
 
     Every rank passes the same global graph and the same NCCL id; make_state
     takes the global y0 and ``state.y`` returns the global Y on every rank.

@@ -125,6 +125,9 @@ void setup_band_grid(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad
   double* dwf = S->mem.upload(wl, S->stream);
   S->row_lo = bp.r0 - bp.lo;
   S->row_hi = bp.r1 - bp.lo;
+  S->part = 1;
+  S->own_vb = static_cast<long>(S->row_lo) * gw;
+  S->own_cnt = (S->row_hi - S->row_lo) * gw;
   S->band_h = gh;
   S->band_w = gw;
   S->band_rad = grad;
@@ -170,6 +173,7 @@ pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pf
     maxrows = std::max(maxrows, b.r1 - b.r0);
   }
   S->band_maxrows = maxrows;
+  S->max_own = maxrows * g->grid_w;
   const int d = S->d;
   S->qr_blocks = qr_blocks_for(S.get(), static_cast<long>(maxrows) * g->grid_w);  // equal on every band
   S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * d * d);
@@ -178,7 +182,7 @@ pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pf
   S->tot_local = S->mem.alloc<double>(3 * pfe_dev::kMaxD);
   S->gathered_a = S->mem.alloc<double>(static_cast<size_t>(nranks) * 3 * d);
   S->gathered_b = S->mem.alloc<double>(static_cast<size_t>(nranks) * d);
-  const size_t rows = static_cast<size_t>(maxrows) * g->grid_w * d;
+  const size_t rows = static_cast<size_t>(S->max_own) * d;
   S->ystage = S->mem.alloc<double>(rows);
   S->yall = S->mem.alloc<double>(rows * nranks);
   S->ensure_log(64);
@@ -208,6 +212,15 @@ void team_sync(Team& t) {
   for (auto* st : t.st) CK(cudaStreamSynchronize(st->s->stream));
 }
 
+// Emulated transport: a device copy ordered on the receiving band's stream
+// (the solver streams are non-blocking, so a legacy-stream copy would not be
+// ordered before the receiver's next kernels).  Callers team_sync() before
+// (sources ready) and after (sources reusable).
+void emu_copy(pfe_solver* dst_owner, double* dst, const double* src, size_t doubles) {
+  if (doubles == 0) return;
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * doubles, cudaMemcpyDeviceToDevice, dst_owner->stream));
+}
+
 // Per-band totals of the producer's partials, then the totals of all bands.
 void team_gather_totals(Team& t, int nq, bool spmv_partials, int nb_producer_of(const pfe_solver*, bool)) {
   const int d = t.S(0)->d, P = t.S(0)->nranks;
@@ -222,8 +235,9 @@ void team_gather_totals(Team& t, int nq, bool spmv_partials, int nb_producer_of(
     for (size_t j = 0; j < t.size(); ++j)
       for (size_t i = 0; i < t.size(); ++i) {
         double* dst = (spmv_partials ? t.S(j)->gathered_b : t.S(j)->gathered_a) + i * cnt;
-        CK(cudaMemcpy(dst, t.S(i)->tot_local, sizeof(double) * cnt, cudaMemcpyDeviceToDevice));
+        emu_copy(t.S(j), dst, t.S(i)->tot_local, cnt);
       }
+    team_sync(t);
     return;
   }
   pfe_solver* S = t.S(0);
@@ -236,7 +250,11 @@ void team_gather_totals(Team& t, int nq, bool spmv_partials, int nb_producer_of(
 // Refreshes the R halo rows of `field` (a [n_local][d] array) from the
 // neighbouring bands.
 template <class F>
+void team_ghosts(Team& t, F&& field);
+
+template <class F>
 void team_halo(Team& t, F&& field) {
+  if (t.S(0)->part == 2) return team_ghosts(t, field);
   const pfe_solver* S0 = t.S(0);
   const int d = S0->d, R = S0->band_rad, W = S0->band_w;
   const size_t blk = static_cast<size_t>(R) * W * d;  // doubles per halo block
@@ -247,10 +265,10 @@ void team_halo(Team& t, F&& field) {
       pfe_state* up = t.st[p - 1];
       pfe_state* dn = t.st[p];
       // dn's top owned rows -> up's bottom halo; up's bottom owned rows -> dn's top halo
-      CK(cudaMemcpy(rows(up, up->s->row_hi), rows(dn, dn->s->row_lo), sizeof(double) * blk,
-                    cudaMemcpyDeviceToDevice));
-      CK(cudaMemcpy(rows(dn, 0), rows(up, up->s->row_hi - R), sizeof(double) * blk, cudaMemcpyDeviceToDevice));
+      emu_copy(up->s, rows(up, up->s->row_hi), rows(dn, dn->s->row_lo), blk);
+      emu_copy(dn->s, rows(dn, 0), rows(up, up->s->row_hi - R), blk);
     }
+    team_sync(t);
     return;
   }
   pfe_state* st = t.st[0];
@@ -302,26 +320,38 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
     }
     team_gather_totals(t, 1, true, nb_producer);
   };
+  const bool ranges = t.S(0)->part == 2;
   int k = 1;
   spmv(1);
   for (;;) {
     pfe_solver* S0 = t.S(0);
     S0->read_ctl();  // every band took the same decision
     if (!S0->h_ctl->any_active || k > maxit) break;
-    if (k > 1) team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
+    if (k > 1 && !ranges) team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
     for (size_t i = 0; i < B; ++i) {
       a[i].phase = pfe_dev::pcg_phase(k);
       t.S(i)->tab->pcg_update(t.S(i)->topo, a[i], t.S(i)->lv());
     }
     team_gather_totals(t, 3, false, nb_producer);
-    team_halo(t, [](pfe_state* st) { return st->r; });
-    spmv(++k);
+    ++k;
+    if (ranges) {
+      // vertex ranges: p' = D^-1 r + beta p on owned rows, then its ghosts
+      for (size_t i = 0; i < B; ++i) {
+        a[i].phase = pfe_dev::pcg_phase(k);
+        a[i].skip_pdir = 1;
+        t.S(i)->tab->pcg_pdir(t.S(i)->topo, a[i], t.S(i)->lv());
+      }
+      team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
+    } else {
+      team_halo(t, [](pfe_state* st) { return st->r; });
+    }
+    spmv(k);
   }
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
     pfe_solver* S = st->s;
-    const long vb = static_cast<long>(S->row_lo) * S->band_w * S->d;
-    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    const long vb = S->own_vb * S->d;
+    const int cnt = S->own_cnt;
     S->tab->pcg_finalize(cnt, st->y + vb, st->y2 + vb, S->ctl, {S->grid_for(static_cast<long>(cnt) * S->d), S->stream, S->sm});
     ++S->inner_launched;
     std::swap(st->y, st->y2);
@@ -336,8 +366,8 @@ void team_split_bregman(Team& t, int max_iter) {
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
     pfe_solver* S = st->s;
-    const long vb = static_cast<long>(S->row_lo) * S->band_w;
-    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    const long vb = S->own_vb;
+    const int cnt = S->own_cnt;
     if (!st->rq_valid) {
       S->tab->rhs_quad(cnt, S->sqd + vb, st->p + vb * S->d, st->breg + vb * S->d, st->rq + vb * S->d,
                        0.5 * S->prm.r, {S->grid_for(static_cast<long>(cnt) * S->d), S->stream, S->sm});
@@ -382,15 +412,16 @@ void team_project(Team& t) {
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
     pfe_solver* S = st->s;
-    const long vb = static_cast<long>(S->row_lo) * S->band_w;
-    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    const long vb = S->own_vb;
+    const int cnt = S->own_cnt;
     S->tab->tsqr_local(cnt, st->y + vb * d, S->sqd + vb, st->breg + vb * d, S->rbuf, {S->qr_blocks, S->stream, S->sm});
   }
   if (t.emulated) {
     team_sync(t);
     for (size_t j = 0; j < B; ++j)
       for (size_t i = 0; i < B; ++i)
-        CK(cudaMemcpy(t.S(j)->rgather + i * fac, t.S(i)->rbuf, sizeof(double) * fac, cudaMemcpyDeviceToDevice));
+        emu_copy(t.S(j), t.S(j)->rgather + i * fac, t.S(i)->rbuf, fac);
+    team_sync(t);
   } else {
     pfe_solver* S = t.S(0);
     nccl_check(nccl().AllGather(S->rbuf, S->rgather, fac, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
@@ -399,8 +430,8 @@ void team_project(Team& t) {
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
     pfe_solver* S = st->s;
-    const long vb = static_cast<long>(S->row_lo) * S->band_w;
-    const int cnt = (S->row_hi - S->row_lo) * S->band_w;
+    const long vb = S->own_vb;
+    const int cnt = S->own_cnt;
     S->tab->tsqr_final(S->nranks * S->qr_blocks, S->rgather, S->wmat, S->ctl, {1, S->stream, S->sm});
     S->tab->project_apply(cnt, st->y + vb * d, S->sqd + vb, st->breg + vb * d, S->wmat, st->p + vb * d,
                           st->rq + vb * d, 0.5 * S->prm.r, {S->grid_for(cnt), S->stream, S->sm});
@@ -424,27 +455,25 @@ void team_run_soc(Team& t, int soc_max, int sb_max) {
   }
 }
 
-// Global column-major Y from the owned rows of every band.
+// Global column-major Y from the owned rows of every band / range.
 void team_gather_y(Team& t, double* out) {
   const pfe_solver* S0 = t.S(0);
-  const int d = S0->d, W = S0->band_w, P = S0->nranks;
+  const int d = S0->d, P = S0->nranks;
   const long gn = S0->global_n;
-  const size_t slot = static_cast<size_t>(S0->band_maxrows) * W * d;
+  const size_t slot = static_cast<size_t>(S0->max_own) * d;
   std::vector<double> all;
   if (t.emulated) {
     all.assign(slot * P, 0.0);
     for (size_t i = 0; i < t.size(); ++i) {
       const pfe_solver* S = t.S(i);
-      const size_t cnt = static_cast<size_t>(S->row_hi - S->row_lo) * W * d;
-      CK(cudaMemcpy(all.data() + i * slot, t.st[i]->y + static_cast<size_t>(S->row_lo) * W * d, sizeof(double) * cnt,
+      CK(cudaMemcpy(all.data() + i * slot, t.st[i]->y + S->own_vb * d, sizeof(double) * S->own_cnt * d,
                     cudaMemcpyDeviceToHost));
     }
   } else {
     pfe_state* st = t.st[0];
     pfe_solver* S = st->s;
-    const size_t cnt = static_cast<size_t>(S->row_hi - S->row_lo) * W * d;
-    CK(cudaMemcpyAsync(S->ystage, st->y + static_cast<size_t>(S->row_lo) * W * d, sizeof(double) * cnt,
-                       cudaMemcpyDeviceToDevice, S->stream));
+    CK(cudaMemcpyAsync(S->ystage, st->y + S->own_vb * d, sizeof(double) * S->own_cnt * d, cudaMemcpyDeviceToDevice,
+                       S->stream));
     nccl_check(nccl().AllGather(S->ystage, S->yall, slot, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
                "ncclAllGather(Y)");
     all.resize(slot * P);
@@ -452,10 +481,18 @@ void team_gather_y(Team& t, double* out) {
     CK(cudaStreamSynchronize(S->stream));
   }
   for (int p = 0; p < P; ++p) {
-    const BandPlan bp = band_plan(S0->band_h, P, S0->band_rad, p);
-    const long v0 = static_cast<long>(bp.r0) * W, cnt = static_cast<long>(bp.r1 - bp.r0) * W;
-    for (long v = 0; v < cnt; ++v)
-      for (int j = 0; j < d; ++j) out[(v0 + v) + j * gn] = all[p * slot + static_cast<size_t>(v) * d + j];
+    long cnt, v0 = 0;
+    if (S0->part == 2) {
+      cnt = S0->range_start[p + 1] - S0->range_start[p];
+    } else {
+      const BandPlan bp = band_plan(S0->band_h, P, S0->band_rad, p);
+      v0 = static_cast<long>(bp.r0) * S0->band_w;
+      cnt = static_cast<long>(bp.r1 - bp.r0) * S0->band_w;
+    }
+    for (long i = 0; i < cnt; ++i) {
+      const long v = S0->part == 2 ? S0->range_vertex[S0->range_start[p] + i] : v0 + i;
+      for (int j = 0; j < d; ++j) out[v + j * gn] = all[p * slot + static_cast<size_t>(i) * d + j];
+    }
   }
 }
 
@@ -469,4 +506,236 @@ void band_timed(pfe_solver* S, F&& f) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
   S->last_ms = ms;
+}
+
+// ------------------------------------------------------ vertex ranges ----
+// General graphs (k-NN) over several GPUs.  The vertices,
+// in the BFS storage order of the whole graph (bfs_storage_order), are cut
+// into contiguous ranges, one per rank.  A rank stores its owned vertices
+// (local rows [0, own)) and then its ghosts -- neighbours owned elsewhere --
+// grouped by owner and in storage order.  Kernels process owned rows only
+// (Csr::vb / ve); ghost rows of p' (after the direction pass) and of Y (after
+// the result selection) are refreshed from their owners.  Every edge incident
+// to an owned vertex is stored locally; an edge crossing two ranges is a
+// replica on both, updated identically (k_sb_pass writes the edges of ghost
+// owners too).  Rows of A and incidence lists keep the reference's term
+// order, so per-vertex arithmetic is that of the single-GPU solver.
+pfe_solver* create_range_solver(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int nranks, int rank,
+                                void* comm) {
+  if (!g || !p) config_error("null graph or params");
+  const auto t0 = std::chrono::steady_clock::now();
+  HostGraph hg{g->n, static_cast<long>(g->m), g->ei, g->ej, g->w, g->degree};
+  validate(hg, *p, true);
+  if (nranks < 1 || rank < 0 || rank >= nranks) config_error("vertex ranges: bad rank / rank count");
+  if (g->n < nranks) config_error("vertex ranges: fewer vertices than ranks");
+  if (g->m > 0x3fffffffL) config_error("graph too large for 32-bit edge indices");
+  auto S = std::make_unique<pfe_solver>();
+  S->prm = *p;
+  S->jacobi_fallback = p->preconditioner == PFE_PRECOND_IC0;
+  init_common(S.get(), x, p->dim);
+  S->persistent = false;
+  S->use_graphs = false;
+  S->nranks = nranks;
+  S->rank = rank;
+  S->comm = comm;
+  S->m = g->m;
+  S->global_n = g->n;
+  S->part = 2;
+  const int n = g->n, P = nranks, d = S->d;
+  const double hl = 0.5 * S->prm.lambda, dterm = 0.5 * S->prm.r;
+  const Incidence inc = build_incidence(hg);
+  const std::vector<int> pos = bfs_storage_order(n, inc.iptr, inc.inbr);
+  std::vector<int> vat(n);
+  for (int v = 0; v < n; ++v) vat[pos[v]] = v;
+  S->range_vertex = vat;
+  S->range_start.resize(P + 1);
+  for (int q = 0; q <= P; ++q) S->range_start[q] = static_cast<int>(static_cast<long>(n) * q / P);
+  const int s0 = S->range_start[rank], s1 = S->range_start[rank + 1], own = s1 - s0;
+  auto owner = [&](int ps) {
+    return static_cast<int>(std::upper_bound(S->range_start.begin(), S->range_start.end(), ps) -
+                            S->range_start.begin()) - 1;
+  };
+  std::vector<int> ghost;  // storage positions of the ghosts, sorted (grouped by owner)
+  std::vector<std::vector<int>> sendl(P);
+  for (int l = 0; l < own; ++l) {
+    const int v = vat[s0 + l];
+    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) {
+      const int pu = pos[inc.inbr[k]];
+      if (pu >= s0 && pu < s1) continue;
+      ghost.push_back(pu);
+      sendl[owner(pu)].push_back(l);
+    }
+  }
+  std::sort(ghost.begin(), ghost.end());
+  ghost.erase(std::unique(ghost.begin(), ghost.end()), ghost.end());
+  const int nloc = own + static_cast<int>(ghost.size());
+  auto lid = [&](int pu) {
+    if (pu >= s0 && pu < s1) return pu - s0;
+    return own + static_cast<int>(std::lower_bound(ghost.begin(), ghost.end(), pu) - ghost.begin());
+  };
+  S->local_vertex.resize(nloc);
+  for (int l = 0; l < nloc; ++l) S->local_vertex[l] = vat[l < own ? s0 + l : ghost[l - own]];
+  // diag(A) from the global incidence (edge order, (r/2) d_v last)
+  std::vector<double> diag(nloc), invd(nloc), deg(nloc), sqd(nloc);
+  for (int l = 0; l < nloc; ++l) {
+    const int v = S->local_vertex[l];
+    double acc = 0.0;
+    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) acc += (hl * inc.iw[k]) * inc.iw[k];
+    diag[l] = acc + dterm * g->degree[v];
+    invd[l] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[l] > 0.0 ? 1.0 / diag[l] : 1.0);
+    deg[l] = g->degree[v];
+    sqd[l] = std::sqrt(g->degree[v]);
+  }
+  // A rows of the owned vertices in the reference's column order
+  std::vector<int> aptr(static_cast<size_t>(own) + 1, 0), acol;
+  std::vector<double> aval;
+  std::vector<std::pair<int, double>> row;
+  for (int l = 0; l < own; ++l) {
+    const int v = S->local_vertex[l];
+    row.clear();
+    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) row.emplace_back(inc.inbr[k], -((hl * inc.iw[k]) * inc.iw[k]));
+    row.emplace_back(v, diag[l]);
+    std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (size_t t = 0; t < row.size();) {
+      const int col = row[t].first;
+      double sum = 0.0;
+      if (col == v) {
+        sum = row[t].second;
+        ++t;
+      } else {
+        for (; t < row.size() && row[t].first == col; ++t) sum += row[t].second;
+      }
+      if (sum != 0.0) {
+        acol.push_back(lid(pos[col]));
+        aval.push_back(sum);
+      }
+    }
+    aptr[l + 1] = static_cast<int>(acol.size());
+  }
+  // local edge rows (first visit order) and incidence lists of the owned vertices
+  std::vector<int> erow(static_cast<size_t>(g->m), -1);
+  std::vector<int> iptr2(static_cast<size_t>(own) + 1, 0), inbr2, ieid2;
+  std::vector<double> iw2;
+  int ne = 0;
+  for (int l = 0; l < own; ++l) {
+    const int v = S->local_vertex[l];
+    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) {
+      const int e = inc.ieid[k], u = inc.inbr[k];
+      if (erow[e] < 0) erow[e] = ne++;
+      inbr2.push_back(lid(pos[u]));
+      ieid2.push_back((erow[e] << 1) | (u > v ? 1 : 0));
+      iw2.push_back(inc.iw[k]);
+    }
+    iptr2[l + 1] = static_cast<int>(inbr2.size());
+  }
+  cudaStream_t st = S->stream;
+  S->n = nloc;
+  S->deg = S->mem.upload(deg, st);
+  S->sqd = S->mem.upload(sqd, st);
+  S->diag = S->mem.upload(diag, st);
+  S->invd = S->mem.upload(invd, st);
+  pfe_dev::Csr c{};
+  c.n = nloc;
+  c.vb = 0;
+  c.ve = own;
+  c.aptr = S->mem.upload(aptr, st);
+  c.acol = S->mem.upload(acol, st);
+  c.aval = S->mem.upload(aval, st);
+  c.iptr = S->mem.upload(iptr2, st);
+  c.inbr = S->mem.upload(inbr2, st);
+  c.ieid = S->mem.upload(ieid2, st);
+  c.iw = S->mem.upload(iw2, st);
+  c.invd = S->invd;
+  S->topo.kind = pfe_host::kTopoCsr;
+  S->topo.csr = c;
+  S->edge_rows = std::max(ne, 1);
+  S->own_vb = 0;
+  S->own_cnt = own;
+  for (int q = 0; q < P; ++q) S->max_own = std::max(S->max_own, S->range_start[q + 1] - S->range_start[q]);
+  // peers: ghost blocks (contiguous, by owner) and send lists (same order)
+  long send_total = 0;
+  for (int q = 0; q < P; ++q) {
+    if (q == rank) continue;
+    auto& sl = sendl[q];
+    std::sort(sl.begin(), sl.end());
+    sl.erase(std::unique(sl.begin(), sl.end()), sl.end());
+    const int r_lo = static_cast<int>(std::lower_bound(ghost.begin(), ghost.end(), S->range_start[q]) - ghost.begin());
+    const int r_hi = static_cast<int>(std::lower_bound(ghost.begin(), ghost.end(), S->range_start[q + 1]) - ghost.begin());
+    if (sl.empty() && r_hi == r_lo) continue;
+    pfe_solver::Peer pr{};
+    pr.rank = q;
+    pr.send_cnt = static_cast<int>(sl.size());
+    pr.send_rows = sl.empty() ? nullptr : S->mem.upload(sl, st);
+    pr.send_off = send_total;
+    pr.recv_off = own + r_lo;
+    pr.recv_cnt = r_hi - r_lo;
+    send_total += pr.send_cnt;
+    S->peers.push_back(pr);
+  }
+  S->sendbuf = S->mem.alloc<double>(static_cast<size_t>(std::max<long>(send_total, 1)) * d);
+  S->qr_blocks = qr_blocks_for(S.get(), S->max_own);  // equal on every rank
+  S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * d * d);
+  S->rgather = S->mem.alloc<double>(static_cast<size_t>(P) * S->qr_blocks * d * d);
+  S->wmat = S->mem.alloc<double>(static_cast<size_t>(d) * d);
+  S->tot_local = S->mem.alloc<double>(3 * pfe_dev::kMaxD);
+  S->gathered_a = S->mem.alloc<double>(static_cast<size_t>(P) * 3 * d);
+  S->gathered_b = S->mem.alloc<double>(static_cast<size_t>(P) * d);
+  S->ystage = S->mem.alloc<double>(static_cast<size_t>(S->max_own) * d);
+  S->yall = S->mem.alloc<double>(static_cast<size_t>(S->max_own) * d * P);
+  S->ensure_log(64);
+  CK(cudaStreamSynchronize(S->stream));
+  S->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return S.release();
+}
+
+// Range state: y0 is the GLOBAL column-major n x d embedding.
+pfe_state* create_range_state(pfe_solver* S, const double* y0_global) {
+  const long gn = S->global_n;
+  std::vector<double> loc(static_cast<size_t>(S->n) * S->d);
+  for (int j = 0; j < S->d; ++j)
+    for (int l = 0; l < S->n; ++l) loc[static_cast<size_t>(j) * S->n + l] = y0_global[S->local_vertex[l] + j * gn];
+  return create_state(S, loc.data());
+}
+
+// Ghost rows of `field` ([n_local][d]) from their owners.
+template <class F>
+void team_ghosts(Team& t, F&& field) {
+  const int d = t.S(0)->d;
+  for (auto* st : t.st) {
+    pfe_solver* S = st->s;
+    for (const auto& pr : S->peers)
+      S->tab->pack_rows(field(st), pr.send_rows, pr.send_cnt, S->sendbuf + pr.send_off * d, S->stream);
+  }
+  if (t.emulated) {
+    team_sync(t);
+    for (size_t i = 0; i < t.size(); ++i) {
+      const pfe_solver* Si = t.S(i);
+      for (const auto& pr : Si->peers) {
+        pfe_state* dst = t.st[pr.rank];
+        for (const auto& back : dst->s->peers) {
+          if (back.rank != Si->rank) continue;
+          if (back.recv_cnt != pr.send_cnt) throw Error(PFE_CUDA_ERROR, "vertex ranges: inconsistent ghost lists");
+          emu_copy(dst->s, field(dst) + static_cast<size_t>(back.recv_off) * d, Si->sendbuf + pr.send_off * d,
+                   static_cast<size_t>(pr.send_cnt) * d);
+        }
+      }
+    }
+    team_sync(t);
+    return;
+  }
+  pfe_state* st = t.st[0];
+  pfe_solver* S = st->s;
+  auto comm = static_cast<ncclComm_t>(S->comm);
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  for (const auto& pr : S->peers) {
+    if (pr.send_cnt > 0)
+      nccl_check(nccl().Send(S->sendbuf + pr.send_off * d, static_cast<size_t>(pr.send_cnt) * d, ncclDouble, pr.rank,
+                             comm, S->stream),
+                 "ncclSend");
+    if (pr.recv_cnt > 0)
+      nccl_check(nccl().Recv(field(st) + static_cast<size_t>(pr.recv_off) * d, static_cast<size_t>(pr.recv_cnt) * d,
+                             ncclDouble, pr.rank, comm, S->stream),
+                 "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
 }

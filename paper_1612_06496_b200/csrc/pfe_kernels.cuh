@@ -56,6 +56,7 @@ struct PcgArgs {
   // Row-band solvers: part_a / part_b hold the per-rank totals gathered from
   // every band ([rank][pair], nb = ranks) instead of this grid's block partials.
   int rank_major;
+  int skip_pdir;  // host side: pcg_spmv does not launch the CSR direction pass
 };
 
 __host__ __device__ __forceinline__ int pcg_phase(int it) { return it == 1 ? 0 : ((it & 1) ? 1 : 2); }
@@ -255,6 +256,17 @@ __global__ void __launch_bounds__(kBlock, 3) k_pcg_init(Topo topo, PcgArgs a) {
     st_row<V>(a.pbuf[0] + static_cast<long>(v) * D + c0, z);
   }
   block_reduce_store<3, D, V>(acc, a.part_a);
+}
+
+// Gathers rows (ghost exchange packing).
+template <int D>
+__global__ void k_pack_rows(const double* __restrict__ src, const int* __restrict__ rows, int cnt,
+                            double* __restrict__ dst) {
+  const long total = static_cast<long>(cnt) * D, stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const long i = e / D;
+    dst[e] = src[static_cast<long>(__ldg(rows + i)) * D + (e - i * D)];
+  }
 }
 
 // ----------------------------------------------- PCG direction (CSR rows) --
@@ -503,7 +515,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sb_pass(Topo topo, SbArgs a) {
       }
       return g;
     };
-    topo.template visitE_b<4>(v, load, [&](int, double w, long slot, bool fwd, const YB& g) {
+    topo.template visitE_b<4>(v, load, [&](int u, double w, long slot, bool fwd, const YB& g) {
       const Row<V>& yu = g.y;
       const Row<V>& bo = g.b;
       Row<V> bn, sv;
@@ -519,7 +531,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_sb_pass(Topo topo, SbArgs a) {
         sv.a[k] = s;
         acc[k] += (fwd ? w : nw) * (s - bn.a[k]);
       }
-      if (fwd) {
+      // the owner (first endpoint) stores b and s; in a vertex-range
+      // partition, edges owned by a ghost vertex are local replicas that this
+      // range updates identically (CSR only: u >= vend() is a ghost row)
+      if (fwd || (!Topo::kGrid && u >= topo.vend())) {
         st_row<V>(a.b_new + slot * D + c0, bn);
         if (a.s_out) st_row<V>(a.s_out + slot * D + c0, sv);
       }

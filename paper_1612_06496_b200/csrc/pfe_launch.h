@@ -80,6 +80,12 @@ struct LaunchTable {
   int (*sb_persistent)(const TopoDesc&, const PersistIn&, Launch);
   // block partials -> nq * D totals (nq = 1 or 3), one block
   void (*local_totals)(int nq, const double* part, int nb, double* out, cudaStream_t);
+  // CSR only: the direction pass p' = D^-1 r + beta p on its own (pcg_spmv
+  // runs it first unless PcgArgs::skip_pdir), for partitioned solvers that
+  // exchange p' ghosts between the two
+  void (*pcg_pdir)(const TopoDesc&, const pfe_dev::PcgArgs&, Launch);
+  // dst[i][D] = src[rows[i]][D] for i < cnt (ghost exchange packing)
+  void (*pack_rows)(const double* src, const int* rows, int cnt, double* dst, cudaStream_t);
 };
 
 const LaunchTable& table_for(int d);  // d in [1, 16]

@@ -99,10 +99,19 @@ struct Impl {
   static void pcg_spmv(const TopoDesc& t, const PcgArgs& a, Launch l) {
     if (t.kind == kTopoGrid1) return grid_spmv<1>(t.g1, a, l);
     if (t.kind == kTopoGrid2) return grid_spmv<2>(t.g2, a, l);
-    if (a.phase != 0) {
+    if (a.phase != 0 && !a.skip_pdir) {
       k_pcg_pdir<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
     }
     k_pcg_spmv<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+  }
+  static void pcg_pdir(const TopoDesc& t, const PcgArgs& a, Launch l) {
+    if (t.kind != kTopoCsr) throw std::runtime_error("pcg_pdir: CSR topologies only");
+    k_pcg_pdir<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+  }
+  static void pack_rows(const double* src, const int* rows, int cnt, double* dst, cudaStream_t s) {
+    if (cnt <= 0) return;
+    const int grid = static_cast<int>(std::min<long>(4096, (static_cast<long>(cnt) * D + kBlock - 1) / kBlock));
+    k_pack_rows<D><<<grid, kBlock, 0, s>>>(src, rows, cnt, dst); PFE_LAUNCHED(__func__);
   }
   static void pcg_update(const TopoDesc& t, const PcgArgs& a, Launch l) {
     on_topo(t, [&](const auto& topo) {
@@ -296,7 +305,9 @@ LaunchTable make_table() {
                      &I::project_apply,
                      &I::max_blocks_per_sm,
                      &I::sb_persistent,
-                     &I::local_totals};
+                     &I::local_totals,
+                     &I::pcg_pdir,
+                     &I::pack_rows};
 }
 
 }  // namespace pfe_host

@@ -229,8 +229,29 @@ struct pfe_solver {
   double* gathered_a = nullptr;   // [ranks][3 d]
   double* gathered_b = nullptr;   // [ranks][d]
   double* rgather = nullptr;      // [ranks * qr_blocks][d][d] TSQR factors of every band
-  double* ystage = nullptr;       // [band_maxrows * band_w][d] owned-row staging for gathers
-  double* yall = nullptr;         // [ranks][band_maxrows * band_w][d]
+  double* ystage = nullptr;       // [max owned rows][d] owned-row staging for gathers
+  double* yall = nullptr;         // [ranks][max owned rows][d]
+  // Multi-GPU partition kind: 0 none, 1 pixel-grid row bands, 2 vertex ranges
+  // of a general graph.  Owned rows are [own_vb, own_vb + own_cnt) of the
+  // local storage; the others are halo (bands) or ghost (ranges) copies.
+  int part = 0;
+  long own_vb = 0;
+  int own_cnt = 0;
+  int max_own = 0;                // largest owned-row count over all ranks
+  // Vertex ranges: ghost exchange with every peer rank.
+  struct Peer {
+    int rank;
+    int send_cnt;      // owned rows the peer holds as ghosts (packed in send order)
+    int* send_rows;    // device list of those local rows
+    long send_off;     // offset (rows) of this peer's block in sendbuf
+    int recv_off;      // local row of the first ghost owned by the peer
+    int recv_cnt;
+  };
+  std::vector<Peer> peers;
+  double* sendbuf = nullptr;      // [sum send_cnt][d]
+  std::vector<int> range_start;   // [ranks + 1] storage-order positions owned by each rank
+  std::vector<int> range_vertex;  // storage-order position -> global vertex
+  std::vector<int> local_vertex;  // local row (owned, then ghosts) -> global vertex
   unsigned long long* trace = nullptr;  // PFE_TRACE=1: phase trace of the persistent kernel
   pfe_params prm{};
   int n = 0;
@@ -396,6 +417,63 @@ int grid_slot(int R, int W, int i, int j) {
   return -1;
 }
 
+// Breadth-first order of the vertices (components in vertex order, neighbours
+// in incidence order): perm[v] = position of v.  Used as the storage order of
+// general graphs and as the basis of vertex-range partitions.
+std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const std::vector<int>& inbr) {
+  std::vector<int> perm(n, -1), queue(n);
+  int next = 0, head = 0;
+  for (int s0 = 0; s0 < n; ++s0) {
+    if (perm[s0] >= 0) continue;
+    perm[s0] = next;
+    queue[next++] = s0;
+    while (head < next) {
+      const int v = queue[head++];
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
+        const int u = inbr[k];
+        if (perm[u] < 0) {
+          perm[u] = next;
+          queue[next++] = u;
+        }
+      }
+    }
+  }
+  return perm;
+}
+
+// Incidence lists in increasing edge index (the row order of M^T).
+struct Incidence {
+  std::vector<int> iptr, inbr, ieid;
+  std::vector<double> iw;
+};
+Incidence build_incidence(const HostGraph& g) {
+  Incidence c;
+  const int n = g.n;
+  const long m = g.m;
+  c.iptr.assign(static_cast<size_t>(n) + 1, 0);
+  for (long k = 0; k < m; ++k) {
+    ++c.iptr[g.ei[k] + 1];
+    ++c.iptr[g.ej[k] + 1];
+  }
+  for (int v = 0; v < n; ++v) c.iptr[v + 1] += c.iptr[v];
+  c.inbr.resize(static_cast<size_t>(2 * m));
+  c.ieid.resize(static_cast<size_t>(2 * m));
+  c.iw.resize(static_cast<size_t>(2 * m));
+  std::vector<int> fill(c.iptr.begin(), c.iptr.end() - 1);
+  for (long k = 0; k < m; ++k) {
+    const int i = g.ei[k], j = g.ej[k];
+    int at = fill[i]++;
+    c.inbr[at] = j;
+    c.ieid[at] = static_cast<int>(k);
+    c.iw[at] = g.w[k];
+    at = fill[j]++;
+    c.inbr[at] = i;
+    c.ieid[at] = static_cast<int>(k);
+    c.iw[at] = g.w[k];
+  }
+  return c;
+}
+
 // Builds the device topology.  Diagonal of A: sum over incident edges in
 // edge order of (hl * w) * w, then + (0.5 r) deg_v last — the accumulation
 // order csr_from_triplets applies to form_normal_matrix's triplets.
@@ -500,28 +578,11 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
 
   // incidence lists in increasing edge index (the row order of M^T)
-  std::vector<int> iptr(static_cast<size_t>(n) + 1, 0);
-  for (long k = 0; k < m; ++k) {
-    ++iptr[g.ei[k] + 1];
-    ++iptr[g.ej[k] + 1];
-  }
-  for (int v = 0; v < n; ++v) iptr[v + 1] += iptr[v];
-  std::vector<int> inbr(static_cast<size_t>(2 * m)), ieid(static_cast<size_t>(2 * m));
-  std::vector<double> iw(static_cast<size_t>(2 * m));
-  {
-    std::vector<int> fill(iptr.begin(), iptr.end() - 1);
-    for (long k = 0; k < m; ++k) {
-      const int i = g.ei[k], j = g.ej[k];
-      int at = fill[i]++;
-      inbr[at] = j;
-      ieid[at] = static_cast<int>(k);
-      iw[at] = g.w[k];
-      at = fill[j]++;
-      inbr[at] = i;
-      ieid[at] = static_cast<int>(k);
-      iw[at] = g.w[k];
-    }
-  }
+  Incidence inc = build_incidence(g);
+  const std::vector<int>& iptr = inc.iptr;
+  const std::vector<int>& inbr = inc.inbr;
+  const std::vector<int>& ieid = inc.ieid;
+  const std::vector<double>& iw = inc.iw;
   std::vector<double> diag(n);
   for (int v = 0; v < n; ++v) {
     double acc = 0.0;
@@ -530,27 +591,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
   // storage order: BFS over the incidence graph (components in vertex order),
   // so the rows a vertex gathers sit near its own and stay in L2 / L1
-  std::vector<int> perm(n, -1), inv(n);
-  {
-    int next = 0, head = 0;
-    std::vector<int> queue(n);
-    for (int s0 = 0; s0 < n; ++s0) {
-      if (perm[s0] >= 0) continue;
-      perm[s0] = next;
-      queue[next++] = s0;
-      while (head < next) {
-        const int v = queue[head++];
-        for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
-          const int u = inbr[k];
-          if (perm[u] < 0) {
-            perm[u] = next;
-            queue[next++] = u;
-          }
-        }
-      }
-    }
-    for (int v = 0; v < n; ++v) inv[perm[v]] = v;
-  }
+  std::vector<int> perm = bfs_storage_order(n, iptr, inbr), inv(n);
+  for (int v = 0; v < n; ++v) inv[perm[v]] = v;
   {
     // diag / inv_diag in storage order ((r/2) d_v is added last, as finish_diag does)
     std::vector<double> dperm(n), invd(n);
@@ -1307,7 +1349,7 @@ int pfe_state_create(pfe_solver* s, const double* y0, pfe_state** out) {
   return guarded([&] {
     if (!y0) config_error("PfeSolver: initial embedding has wrong shape");
     CK(cudaSetDevice(s->device));
-    *out = s->band_w ? create_band_state(s, y0) : create_state(s, y0);
+    *out = s->part == 1 ? create_band_state(s, y0) : (s->part == 2 ? create_range_state(s, y0) : create_state(s, y0));
   });
 }
 
@@ -1325,7 +1367,7 @@ int pfe_state_get(pfe_state* st, int32_t field, double* out) {
     pfe_solver* S = st->s;
     CK(cudaSetDevice(S->device));
     const int d = S->d;
-    if (S->band_w) {  // row-band solver: the global Y, gathered from every band
+    if (S->part) {  // partitioned solver: the global Y, gathered from every band / range
       if (field != PFE_FIELD_Y) config_error("row-band solvers expose the gathered embedding Y only");
       Team t{{st}, false};
       team_gather_y(t, out);
@@ -1355,7 +1397,7 @@ int pfe_state_set(pfe_state* st, int32_t field, const double* in) {
     pfe_solver* S = st->s;
     CK(cudaSetDevice(S->device));
     const int d = S->d;
-    if (S->band_w) config_error("row-band solvers take their state from make_state only");
+    if (S->part) config_error("partitioned (multi-GPU) solvers take their state from make_state only");
     if (field <= PFE_FIELD_BREGMAN) {
       double* dst = field == PFE_FIELD_Y ? st->y : (field == PFE_FIELD_P ? st->p : st->breg);
       upload_rows(S, in, S->n, d, dst, st->q);
@@ -1384,7 +1426,7 @@ int pfe_split_bregman(pfe_solver* s, pfe_state* st, int32_t max_iter, pfe_iterat
   return guarded([&] {
     CK(cudaSetDevice(s->device));
     if (max_iter <= 0) return;
-    if (s->band_w) {
+    if (s->part) {
       if (cb || s->prm.conv_tol > 0.0) config_error("row-band solvers run fixed iteration counts without callbacks");
       Team t{{st}, false};
       s->ensure_log(max_iter);
@@ -1400,7 +1442,7 @@ int pfe_run_soc(pfe_solver* s, pfe_state* st, int32_t soc_max, int32_t sb_max) {
   return guarded([&] {
     CK(cudaSetDevice(s->device));
     if (soc_max <= 0) return;
-    if (s->band_w) {
+    if (s->part) {
       if (s->prm.conv_tol > 0.0) config_error("row-band solvers run fixed iteration counts (conv_tol = 0)");
       Team t{{st}, false};
       band_timed(s, [&] { team_run_soc(t, soc_max, std::max(0, sb_max)); });
@@ -1413,7 +1455,7 @@ int pfe_run_soc(pfe_solver* s, pfe_state* st, int32_t soc_max, int32_t sb_max) {
 int pfe_two_stage(pfe_solver* s, pfe_state* st) {
   return guarded([&] {
     CK(cudaSetDevice(s->device));
-    if (s->band_w) {
+    if (s->part) {
       if (s->prm.conv_tol > 0.0) config_error("row-band solvers run fixed iteration counts (conv_tol = 0)");
       Team t{{st}, false};
       band_timed(s, [&] {
@@ -1651,7 +1693,8 @@ int pfe_solver_create_band(const pfe_graph* g, const pfe_params* p, const pfe_ex
       nccl_check(nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
     }
     try {
-      *out = create_band_solver(g, p, x, nranks, rank, comm);
+      *out = g && g->grid_h > 0 ? create_band_solver(g, p, x, nranks, rank, comm)
+                                : create_range_solver(g, p, x, nranks, rank, comm);
     } catch (...) {
       if (comm) nccl().CommDestroy(comm);
       throw;
@@ -1667,8 +1710,11 @@ int pfe_solve_banded(const pfe_graph* g, const pfe_params* p, const pfe_exec* x,
     Team t;
     t.emulated = true;
     for (int b = 0; b < nbands; ++b) {
-      solvers.emplace_back(create_band_solver(g, p, x, nbands, b, nullptr));
-      states.emplace_back(create_band_state(solvers.back().get(), y0));
+      const bool grid = g && g->grid_h > 0;
+      solvers.emplace_back(grid ? create_band_solver(g, p, x, nbands, b, nullptr)
+                                : create_range_solver(g, p, x, nbands, b, nullptr));
+      states.emplace_back(grid ? create_band_state(solvers.back().get(), y0)
+                               : create_range_state(solvers.back().get(), y0));
       t.st.push_back(states.back().get());
     }
     team_run_soc(t, p->soc_max, p->sb_max_stage1);

@@ -151,3 +151,140 @@ def test_banded_pcg_two_ranks_gloo(tmp_path):
         r0, r1 = int(arr[0]), int(arr[1])
         got[r0 * W:r1 * W] = arr[2:]
     assert np.abs(got - full).max() <= 1e-12 * np.abs(full).max()
+
+
+# ------------------------------------------------------------ vertex ranges --
+def bfs_order(n, nbrs):
+    """Storage order of the library's general-graph path (bfs_storage_order)."""
+    pos = -np.ones(n, np.int64)
+    nxt = 0
+    queue = []
+    for s0 in range(n):
+        if pos[s0] >= 0:
+            continue
+        pos[s0] = nxt
+        nxt += 1
+        queue.append(s0)
+        while queue:
+            v = queue.pop(0)
+            for u in nbrs[v]:
+                if pos[u] < 0:
+                    pos[u] = nxt
+                    nxt += 1
+                    queue.append(u)
+    return pos
+
+
+def range_problem():
+    from conftest import random_graph
+
+    rng = np.random.Generator(np.random.PCG64(9))
+    g = random_graph(90, 200, rng)
+    b = rng.normal(size=g.n)
+    x0 = rng.normal(size=g.n)
+    return g, b, x0
+
+
+def ranged_pcg(rank, P, g, b_glob, x0_glob, iters, comm):
+    """Jacobi-PCG on vertex range `rank` with the library's ghost schedule:
+    owned vertices first, ghosts grouped by owner in storage order; p' is
+    formed on owned rows and its ghosts exchanged before each SpMV."""
+    A, diag = operator(g)
+    nbrs = [[] for _ in range(g.n)]
+    for i, j in zip(g.ei, g.ej):  # incidence in edge order
+        nbrs[i].append(j)
+        nbrs[j].append(i)
+    pos = bfs_order(g.n, nbrs)
+    vat = np.argsort(pos)
+    starts = [g.n * q // P for q in range(P + 1)]
+    owner = lambda ps: int(np.searchsorted(starts, ps, side="right") - 1)
+    s0, s1 = starts[rank], starts[rank + 1]
+    own = vat[s0:s1]
+    ghost_pos = sorted({int(pos[u]) for v in own for u in nbrs[v] if not (s0 <= pos[u] < s1)})
+    local = np.concatenate([own, vat[ghost_pos]]).astype(np.int64) if ghost_pos else own
+    nown = len(own)
+    A_loc = A[own][:, local]
+    invd = 1.0 / diag[local]
+    # exchange lists (rank -> peer): owned local rows adjacent to the peer's vertices
+    send = {q: sorted({l for l, v in enumerate(own) for u in nbrs[v] if owner(pos[u]) == q})
+            for q in range(P) if q != rank}
+    recv = {q: [k + nown for k, ps in enumerate(ghost_pos) if owner(ps) == q] for q in range(P) if q != rank}
+
+    def ghosts(vec):
+        if comm is None:
+            return
+        import torch
+
+        reqs, bufs = [], {}
+        for q in send:
+            if send[q]:
+                reqs.append(dist.isend(torch.from_numpy(vec[send[q]].copy()), q))
+            if recv[q]:
+                bufs[q] = torch.empty(len(recv[q]), dtype=torch.float64)
+                reqs.append(dist.irecv(bufs[q], q))
+        for r in reqs:
+            r.wait()
+        for q, t in bufs.items():
+            vec[recv[q]] = t.numpy()
+
+    def total(*vals):
+        import torch
+
+        mine = torch.tensor(vals, dtype=torch.float64)
+        if comm is None:
+            return list(mine.numpy())
+        allv = [torch.empty_like(mine) for _ in range(P)]
+        dist.all_gather(allv, mine)
+        s = np.zeros(len(vals))
+        for v in allv:
+            s = s + v.numpy()
+        return list(s)
+
+    o = slice(0, nown)
+    x = x0_glob[local].copy()
+    bb = b_glob[local]
+    r = np.zeros_like(x)
+    r[o] = bb[o] - A_loc @ x
+    p = np.zeros_like(x)
+    p[o] = invd[o] * r[o]
+    _, _, rz = total(bb[o] @ bb[o], r[o] @ r[o], r[o] @ p[o])
+    ghosts(p)
+    beta = 0.0
+    for k in range(1, iters + 1):
+        if k > 1:
+            p[o] = invd[o] * r[o] + beta * p[o]
+            ghosts(p)
+        q = A_loc @ p
+        (pq,) = total(p[o] @ q)
+        alpha = rz / pq
+        x[o] = x[o] + alpha * p[o]
+        r[o] = r[o] - alpha * q
+        _, rz_new = total(r[o] @ r[o], r[o] @ (invd[o] * r[o]))
+        beta = rz_new / rz
+        rz = rz_new
+    return x[o], own
+
+
+def _range_worker(rank, P, port, res_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    g, b, x0 = range_problem()
+    xs, own = ranged_pcg(rank, P, g, b, x0, 10, True)
+    np.save(f"{res_path}_{rank}.npy", np.stack([own.astype(np.float64), xs]))
+    dist.destroy_process_group()
+
+
+def test_vertex_range_pcg_two_ranks_gloo(tmp_path):
+    P = 2
+    res = str(tmp_path / "v")
+    mp.spawn(_range_worker, args=(P, free_port(), res), nprocs=P, join=True)
+    g, b, x0 = range_problem()
+    full, own = ranged_pcg(0, 1, g, b, x0, 10, None)
+    ref = np.zeros(g.n)
+    ref[own] = full
+    got = np.zeros(g.n)
+    for rank in range(P):
+        arr = np.load(f"{res}_{rank}.npy")
+        got[arr[0].astype(np.int64)] = arr[1]
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()

@@ -65,3 +65,44 @@ def test_band_rejects_non_grid_and_thin_bands():
     y0 = api.random_embedding(g.n, 2, 1, g.degree)
     with pytest.raises(api.ConfigError, match="at least R image rows"):
         api.soc_banded(g, prm, y0, 4)
+
+
+# ----------------------------------------------------------- vertex ranges --
+def knn_points_graph(n, k, seed):
+    from paper_1612_06496_b200.inputs import knn_graph
+
+    rng = np.random.Generator(np.random.PCG64(seed))
+    pts = rng.uniform(-1.0, 1.0, size=(n, 3))
+    return knn_graph(pts, k)
+
+
+@pytest.mark.parametrize("nparts,d", [(2, 4), (3, 3), (4, 8), (5, 16)])
+def test_vertex_ranges_match_single_domain(nparts, d):
+    """General (k-NN) graphs split into vertex ranges with ghost rows: same
+    result as the single-domain solver up to the reduction order."""
+    g = knn_points_graph(1500, 8, 20 + nparts)
+    prm = params(d)
+    y0 = api.random_embedding(g.n, d, 3, g.degree)
+    single = api.soc(g, prm, y0)
+    ranged = api.soc_banded(g, prm, y0, nparts)
+    assert rel(ranged, single) <= 1e-11
+    assert rel(ranged, O.solve(g, prm, y0, mode=0)) <= 1e-10
+
+
+def test_vertex_ranges_two_stage_disconnected_and_repeatable():
+    """Two components (a range may own vertices of both), Stage II on, bitwise repeatable."""
+    from conftest import random_graph
+
+    rng = np.random.Generator(np.random.PCG64(5))
+    a = random_graph(120, 300, rng)
+    b = random_graph(80, 200, rng)
+    ei = np.concatenate([a.ei, b.ei + a.n])
+    ej = np.concatenate([a.ej, b.ej + a.n])
+    w = np.concatenate([a.w, b.w])
+    g = api.WeightedGraph(a.n + b.n, ei, ej, w, np.concatenate([a.degree, b.degree]))
+    prm = params(3, soc=2, sb=4, stage2=5)
+    y0 = api.random_embedding(g.n, 3, 4, g.degree)
+    r1 = api.soc_banded(g, prm, y0, 3, two_stage=True)
+    r2 = api.soc_banded(g, prm, y0, 3, two_stage=True)
+    assert np.array_equal(r1, r2)
+    assert rel(r1, api.pfe_two_stage(g, prm, y0)) <= 1e-11
