@@ -240,6 +240,13 @@ int pfe_random_embedding(int32_t n, int32_t d, uint64_t seed, const double* degr
 int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
                int32_t* labels);
 
+/* pfe_kmeans on the GPU: same seeding random stream,
+ * tie-breaks, empty-cluster split and stop rule as pfe_kmeans; distances are
+ * bitwise the host's, sums associate by chunks of 4096 points (labels agree
+ * with the host's up to ties).  d <= 16, k * d <= 6144. */
+int pfe_kmeans_device(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
+                      int32_t device, int32_t* labels);
+
 /* k-NN graph builder for point sets (configs C1 / C5).  No reference
  * counterpart: the reference has no k-NN builder; this
  * is the harness definition of paper_1612_06496_b200/inputs.py knn_graph --

@@ -463,15 +463,23 @@ def d_orthonormalize(a, degree) -> np.ndarray:
     return _from_colmajor(out, n, d)
 
 
-def kmeans(points, k: int, seed: int, max_iter: int = 100) -> np.ndarray:
-    """kmeans (cluster.cpp:54-124): k-means++ seeding + Lloyd; returns labels."""
+def kmeans(points, k: int, seed: int, max_iter: int = 100, device: Optional[int] = None) -> np.ndarray:
+    """kmeans (cluster.cpp:54-124): k-means++ seeding + Lloyd; returns labels.
+
+    ``device=None`` runs the host implementation (pfe_kmeans); a device
+    ordinal runs the O(n k d) work on that GPU (pfe_kmeans_device) with the
+    same random stream and rules."""
     pts = np.asarray(points, dtype=np.float64)
     if pts.ndim == 1:
         pts = pts.reshape(-1, 1)
     n, d = pts.shape
     pc = _colmajor(pts)
     lab = np.zeros(n, np.int32)
-    _check(N.load().pfe_kmeans(n, d, N.dptr(pc), int(k), int(seed), int(max_iter), N.iptr(lab)))
+    if device is None:
+        _check(N.load().pfe_kmeans(n, d, N.dptr(pc), int(k), int(seed), int(max_iter), N.iptr(lab)))
+    else:
+        _check(N.load().pfe_kmeans_device(n, d, N.dptr(pc), int(k), int(seed), int(max_iter), int(device),
+                                          N.iptr(lab)))
     return lab
 
 

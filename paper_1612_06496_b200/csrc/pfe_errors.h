@@ -17,6 +17,7 @@ void random_embedding(int n, int d, uint64_t seed, const double* deg, double* ou
 void d_orthonormalize(int n, int d, const double* a, const double* deg, double* out);
 void kmeans(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
 void knn_search(int n, int dim, const double* pts, int k, double* d2, int32_t* idx);
+void kmeans_device(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
 long knn_graph_from_lists(int n, int k, const double* d2, const int32_t* idx, int32_t* ei, int32_t* ej, double* w,
                           double* degree, double* sigma_out);
 

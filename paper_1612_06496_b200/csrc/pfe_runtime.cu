@@ -1764,6 +1764,14 @@ int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t s
   return guarded([&] { pfe_host::kmeans(n, d, points, k, seed, max_iter, labels); });
 }
 
+int pfe_kmeans_device(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
+                      int32_t device, int32_t* labels) {
+  return guarded([&] {
+    require_device(device);
+    pfe_host::kmeans_device(n, d, points, k, seed, max_iter, labels);
+  });
+}
+
 int pfe_knn_graph(int32_t n, int32_t dim, const double* points, int32_t k, int32_t device, int32_t* ei, int32_t* ej,
                   double* w, double* degree, int64_t* m_out, double* sigma_out) {
   return guarded([&] {
