@@ -93,7 +93,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int D, int R>
-__global__ void __launch_bounds__(256, 2) k_sb_persistent(PersistArgs<R> a) {
+__global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persistent(PersistArgs<R> a) {
   using G = TileGeo<R, D>;
   using T = GridTopo<R>;
   constexpr int V = G::V;

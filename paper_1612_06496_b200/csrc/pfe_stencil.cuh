@@ -42,7 +42,9 @@ struct TileGeo {
   static constexpr int TW = 32;
   static constexpr int TH = (D <= 4 || R == 2) ? 8 : 4;  // keeps the sb staging at >= 3 blocks/SM
   static constexpr int NV = TW * TH;                     // tile vertices
-  static constexpr int NT = 256;                         // threads per block
+  // threads per block: 5x5 tiles need ~100-200 KB of shared memory (one
+  // block per SM), so they get 16 warps to keep enough loads in flight
+  static constexpr int NT = R == 2 ? 512 : 256;
   static constexpr int HW = TW + 2 * R, HH = TH + 2 * R, NP = HW * HH;
   static constexpr int S = GridTopo<R>::S;
   static constexpr int NO = (TH + R) * HW;  // positions owning edges that touch the tile
