@@ -170,20 +170,31 @@ __device__ __forceinline__ double tile_apply_A(double hl, const double* P, const
                                                double diag_v) {
   using G = TileGeo<R, D>;
   using T = GridTopo<R>;
-  double q = 0.0;
+  // branch-free: every term is loaded and formed, absent edges (w == 0) are
+  // skipped by a select, so all loads are in flight before the serial
+  // reference-order additions
+  double t[2 * G::S + 1];
+  bool nz[2 * G::S + 1];
 #pragma unroll
-  for (int s = G::S - 1; s >= 0; --s) {
+  for (int j = 0; j < G::S; ++j) {
+    const int s = G::S - 1 - j;
     const int npos = hpos - T::dy(s) * G::HW - T::dx(s);
     const double w = Wt[s * G::NP + npos];
-    if (w != 0.0) q += -((hl * w) * w) * P[npos * D + c];
+    nz[j] = w != 0.0;
+    t[j] = -((hl * w) * w) * P[npos * D + c];
   }
-  q += diag_v * P[hpos * D + c];
+  nz[G::S] = true;
+  t[G::S] = diag_v * P[hpos * D + c];
 #pragma unroll
   for (int s = 0; s < G::S; ++s) {
     const int npos = hpos + T::dy(s) * G::HW + T::dx(s);
     const double w = Wt[s * G::NP + hpos];
-    if (w != 0.0) q += -((hl * w) * w) * P[npos * D + c];
+    nz[G::S + 1 + s] = w != 0.0;
+    t[G::S + 1 + s] = -((hl * w) * w) * P[npos * D + c];
   }
+  double q = 0.0;
+#pragma unroll
+  for (int j = 0; j < 2 * G::S + 1; ++j) q = nz[j] ? q + t[j] : q;
   return q;
 }
 
