@@ -4,7 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
-#include <iostream>
+#include <cstdio>
 #include <limits>
 #include <map>
 #include <random>
@@ -632,8 +632,10 @@ void sb_loop(State& st, int max_iter, const IterCb& cb, const Csr& m, const Csr&
     for (size_t j = 0; j < reps.size(); ++j) {
       kmax = std::max(kmax, reps[j].iterations);
       if (warn && !reps[j].converged)
-        std::cerr << "pfe: inner solve column " << j << " stopped at rel residual "
-                  << reps[j].final_rel_residual << "\n";
+        // stdio, not iostream: a ctypes-loaded oracle can share the process
+        // with another libstdc++ whose locale facets crash num_put
+        std::fprintf(stderr, "pfe: inner solve column %zu stopped at rel residual %g\n", j,
+                     reps[j].final_rel_residual);
     }
     if (log) {
       log->pcg_iters.push_back(kmax);
