@@ -136,12 +136,15 @@ void setup_band_grid(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad
   S->band_lo = bp.lo;
   S->edge_rows = nl * S_;
   const int hloc = bp.hi - bp.lo;
+  double* dcf = grid_coef(S, dwf, nl * S_, hl, S->stream);
   if (grad == 1) {
     S->topo.kind = pfe_host::kTopoGrid1;
     S->topo.g1 = pfe_dev::Grid<1>{S->n, hloc, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+    S->topo.g1.cf = dcf;
   } else {
     S->topo.kind = pfe_host::kTopoGrid2;
     S->topo.g2 = pfe_dev::Grid<2>{S->n, hloc, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+    S->topo.g2.cf = dcf;
   }
 }
 
@@ -307,6 +310,7 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
     a[i].rd_a = S->gathered_a;
     a[i].rd_b = S->gathered_b;
     a[i].rank_major = 1;
+    a[i].totals = 0;  // per-band totals are gathered across ranks instead
     a[i].nb_init = a[i].nb_update = a[i].nb_spmv = S->nranks;
   }
   const int maxit = t.S(0)->prm.pcg_max_iter;

@@ -162,6 +162,9 @@ struct Grid {
   // outside [row_lo, row_hi) are a halo copied from neighbouring row bands.
   // A single-GPU solver owns every row.
   int row_lo, row_hi;
+  // [n][S] off-diagonal entries of A per forward slot, -((hl w) w), +0.0 for
+  // an absent edge (tiled stencil kernels; set by the host after construction)
+  const double* __restrict__ cf = nullptr;
   __device__ __forceinline__ double inv_diag(int v) const { return __ldg(invd + v); }
   __device__ __forceinline__ int vbeg() const { return row_lo * W; }
   __device__ __forceinline__ int vend() const { return row_hi * W; }
@@ -258,53 +261,73 @@ struct Csr {
       f(__ldg(inbr + k), __ldg(iw + k), static_cast<long>(code >> 1), (code & 1) != 0);
     }
   }
-  // Batched visits for gather-bound k-NN rows: the index loads of a batch of
-  // B entries, then their B gathers load(...), are all issued before
-  // use(...) consumes them in row / edge order (the summation order is
-  // unchanged; only the memory round trips overlap).
+  // Batched visits for gather-bound k-NN rows: a batch's B gathers load(...)
+  // (and its weights) are all issued before use(...) consumes them in row /
+  // edge order (the summation order is unchanged; only the memory round
+  // trips overlap).  The neighbour indices of the next batch are loaded
+  // before the current batch is consumed, so each batch costs one dependent
+  // round trip (its gathers), not two.
   template <int B, class L, class F>
   __device__ __forceinline__ void visitA_b(int v, L&& load, F&& use) const {
     const int b = __ldg(aptr + v), e = __ldg(aptr + v + 1);
-    for (int k0 = b; k0 < e; k0 += B) {
-      using G = decltype(load(0));
-      int cu[B];
-      double av[B];
-      G g[B];
+    using G = decltype(load(0));
+    int cu[B];
 #pragma unroll
-      for (int j = 0; j < B; ++j) {
-        const bool ok = k0 + j < e;
-        cu[j] = ok ? __ldg(acol + k0 + j) : -1;
-        av[j] = ok ? __ldg(aval + k0 + j) : 0.0;
-      }
+    for (int j = 0; j < B; ++j) cu[j] = b + j < e ? __ldg(acol + b + j) : -1;
+    for (int k0 = b; k0 < e; k0 += B) {
+      G g[B];
+      double av[B];
 #pragma unroll
       for (int j = 0; j < B; ++j)
-        if (cu[j] >= 0) g[j] = load(cu[j]);
+        if (cu[j] >= 0) {
+          g[j] = load(cu[j]);
+          av[j] = __ldg(aval + k0 + j);
+        }
+      int cn[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) cn[j] = k0 + B + j < e ? __ldg(acol + k0 + B + j) : -1;
 #pragma unroll
       for (int j = 0; j < B; ++j)
         if (cu[j] >= 0) use(av[j], g[j]);
+#pragma unroll
+      for (int j = 0; j < B; ++j) cu[j] = cn[j];
     }
   }
   template <int B, class L, class F>
   __device__ __forceinline__ void visitE_b(int v, L&& load, F&& use) const {
     const int b = __ldg(iptr + v), e = __ldg(iptr + v + 1);
+    using G = decltype(load(0, 0L));
+    int cu[B], cc[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const bool ok = b + j < e;
+      cu[j] = ok ? __ldg(inbr + b + j) : -1;
+      cc[j] = ok ? __ldg(ieid + b + j) : 0;
+    }
     for (int k0 = b; k0 < e; k0 += B) {
-      using G = decltype(load(0, 0L));
-      int cu[B], cc[B];
-      double cw[B];
       G g[B];
+      double cw[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) {
+          g[j] = load(cu[j], static_cast<long>(cc[j] >> 1));
+          cw[j] = __ldg(iw + k0 + j);
+        }
+      int un[B], cn[B];
 #pragma unroll
       for (int j = 0; j < B; ++j) {
-        const bool ok = k0 + j < e;
-        cu[j] = ok ? __ldg(inbr + k0 + j) : -1;
-        cc[j] = ok ? __ldg(ieid + k0 + j) : 0;
-        cw[j] = ok ? __ldg(iw + k0 + j) : 0.0;
+        const bool ok = k0 + B + j < e;
+        un[j] = ok ? __ldg(inbr + k0 + B + j) : -1;
+        cn[j] = ok ? __ldg(ieid + k0 + B + j) : 0;
       }
 #pragma unroll
       for (int j = 0; j < B; ++j)
-        if (cu[j] >= 0) g[j] = load(cu[j], static_cast<long>(cc[j] >> 1));
-#pragma unroll
-      for (int j = 0; j < B; ++j)
         if (cu[j] >= 0) use(cu[j], cw[j], static_cast<long>(cc[j] >> 1), (cc[j] & 1) != 0, g[j]);
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        cu[j] = un[j];
+        cc[j] = cn[j];
+      }
     }
   }
 };

@@ -57,6 +57,14 @@ struct PcgArgs {
   // every band ([rank][pair], nb = ranks) instead of this grid's block partials.
   int rank_major;
   int skip_pdir;  // host side: pcg_spmv does not launch the CSR direction pass
+  // Producer-side totals (single-domain solvers): the last block of each
+  // producer reduces the block partials in a fixed order and writes the NQ*D
+  // totals to tot_a (init / update) or tot_b (spmv); consumers then read
+  // those (rd_* = tot_*, nb = 1) instead of every block re-reducing all
+  // partials, which costs nb^2 loads (dominant for 10^3-block grids).
+  double* tot_a;
+  double* tot_b;
+  int totals;
 };
 
 __host__ __device__ __forceinline__ int pcg_phase(int it) { return it == 1 ? 0 : ((it & 1) ? 1 : 2); }
@@ -64,6 +72,19 @@ __device__ __forceinline__ double* pcg_pnew(const PcgArgs& a) { return a.phase =
 __device__ __forceinline__ const double* pcg_pold(const PcgArgs& a) { return a.phase == 1 ? a.pbuf[1] : a.pbuf[0]; }
 
 constexpr double kInf = __builtin_huge_val();
+
+// Producer epilogue: block partials, then (a.totals) the grid totals written
+// by the last block to arrive (deterministic fixed-order reduction).
+template <int NQ, int D, int V, int NT = kBlock>
+__device__ __forceinline__ void store_partials(const PcgArgs& a, double (&acc)[NQ][V], double* __restrict__ partials,
+                                               double* __restrict__ tot) {
+  block_reduce_store<NQ, D, V, NT>(acc, partials);
+  if (a.totals) {
+    __shared__ double out[NQ][D];
+    if (grid_reduce_last<NQ, D, NT>(partials, a.ctl, out) && threadIdx.x < NQ * D)
+      tot[threadIdx.x] = out[threadIdx.x / D][threadIdx.x % D];
+  }
+}
 
 // Block-wide fixed-order reduction of a producer's pair-major partials
 // (nb blocks x NQ*D pairs) into shared out[NQ][D]; all NT threads take part.
@@ -255,7 +276,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_pcg_init(Topo topo, PcgArgs a) {
     st_row<V>(a.r + static_cast<long>(v) * D + c0, r);
     st_row<V>(a.pbuf[0] + static_cast<long>(v) * D + c0, z);
   }
-  block_reduce_store<3, D, V>(acc, a.part_a);
+  store_partials<3, D, V>(a, acc, a.part_a, a.tot_a);
 }
 
 // Gathers rows (ghost exchange packing).
@@ -359,7 +380,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_pcg_spmv(Topo topo, PcgArgs a) {
     }
     st_row<V>(a.q + static_cast<long>(v) * D + c0, qv);
   }
-  block_reduce_store<1, D, V>(acc, a.part_b);
+  store_partials<1, D, V>(a, acc, a.part_b, a.tot_b);
 }
 
 // ----------------------------------------------------------- PCG update -----
@@ -414,7 +435,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(Topo topo, PcgArgs a) {
     st_row<V>(a.r + o, r);
     if (e + stride < total) load(e + stride);
   }
-  block_reduce_store<3, D, V>(acc, a.part_a);
+  store_partials<3, D, V>(a, acc, a.part_a, a.tot_a);
 }
 
 // --------------------------------------------------------- PCG finalize -----

@@ -83,7 +83,8 @@ struct PersistGeo {
   using G = TileGeo<R, D>;
   static constexpr int kInit2 = 2 * G::kInit, kSpmv2 = 2 * G::kSpmv;
   static constexpr int kA = kInit2 > kSpmv2 ? kInit2 : kSpmv2;
-  static constexpr int kSmem = kA > G::kSb ? kA : G::kSb;  // doubles
+  static constexpr int kSbB = G::kStageB ? G::kSb : 2 * G::kSb;  // sb phase (double-buffered for 5x5)
+  static constexpr int kSmem = kA > kSbB ? kA : kSbB;  // doubles
 };
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
@@ -124,12 +125,12 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
       auto stage = [&](int t, int buf) {
         double* P = smem + buf * G::kInit;
         double* Wt = P + G::NP * D;
-        double* Bv = Wt + G::S * G::NP;
+        double* Bv = Wt + G::S * G::NPW;
         double* Dg = Bv + G::NV * D;
         double* Iv = Dg + G::NV;
         const TileIdx ti = tile_of<R, D>(g, t);
         stage_rows<R, D, D>(g, ti, x0, P, G::HH);
-        stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+        stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
         stage_interior<R, D, D>(g, ti, rhs, Bv);
         stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         stage_interior<R, D, 1>(g, ti, g.invd, Iv);
@@ -144,12 +145,12 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
         __syncthreads();
         const double* P = smem + buf * G::kInit;
         const double* Wt = P + G::NP * D;
-        const double* Bv = Wt + G::S * G::NP;
+        const double* Bv = Wt + G::S * G::NPW;
         const double* Dg = Bv + G::NV * D;
         const double* Iv = Dg + G::NV;
         const TileIdx ti = tile_of<R, D>(g, t);
         for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-          const double ax = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
+          const double ax = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
           const double b = Bv[tv * D + c];
           const double rr = b - ax;
           const double z = Iv[tv] * rr;
@@ -210,14 +211,14 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
           double* Rs = P + G::NP * D;
           double* Iv = Rs + G::NP * D;
           double* Wt = Iv + G::NP;
-          double* Dg = Wt + G::S * G::NP;
+          double* Dg = Wt + G::S * G::NPW;
           const TileIdx ti = tile_of<R, D>(g, t);
           stage_rows<R, D, D>(g, ti, pold, P, G::HH);
           if (!first) {
             stage_rows<R, D, D>(g, ti, a.r, Rs, G::HH);
             stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
           }
-          stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+          stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
           stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         };
         int buf = 0;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
           const double* Rs = P + G::NP * D;
           const double* Iv = Rs + G::NP * D;
           const double* Wt = Iv + G::NP;
-          const double* Dg = Wt + G::S * G::NP;
+          const double* Dg = Wt + G::S * G::NPW;
           if (!first) {
             for (int e = threadIdx.x; e < G::NP * D; e += NT) {
               const int pos = e / D, c = e - pos * D;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
           }
           const TileIdx ti = tile_of<R, D>(g, t);
           for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-            const double qv = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
+            const double qv = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
             const double pv = P[hpos * D + c];
             a.q[v * D + c] = qv;
             if (!first) pnew[v * D + c] = pv;
@@ -403,54 +404,52 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
       double* b_new = a.eb[ebcur ^ 1];
       double* s_out = (last && a.write_s_last) ? a.es : nullptr;
       double* rhs_out = (!last || a.rhs_last) ? a.r : nullptr;
-      double* P = smem;
-      double* Wt = P + G::NP * D;
-      double* Rq = Wt + G::S * G::NP;
-      double* Bo = Rq + G::NV * D;
-      for (int t = blockIdx.x; t < nt; t += nb) {
+      // 8-neighbour grids stage b_old (the tile fills shared memory: single
+      // buffer); 5x5 grids read b_old from global memory and double-buffer
+      // the tile staging like the SpMV
+      constexpr bool kDB = !G::kStageB;
+      auto stage = [&](int t, int buf) {
+        double* P = smem + buf * G::kSb;
+        double* Wt = P + G::NP * D;
+        double* Rq = Wt + G::S * G::NPW;
+        double* Bo = Rq + G::NV * D;
         const TileIdx ti = tile_of<R, D>(g, t);
         stage_rows<R, D, D>(g, ti, y, P, G::HH);
-        stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+        stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH, G::NPW);
         if (rhs_out) stage_interior<R, D, D>(g, ti, a.rq, Rq);
         if constexpr (G::kStageB) {
-          if (b_old) stage_planes<R, D, G::S, D>(g, ti, b_old, Bo, G::TH + R);
+          if (b_old) stage_planes<R, D, G::S, D>(g, ti, b_old, Bo, G::TH + R, G::NO);
         }
-        cp_async_wait_all();
+      };
+      int buf = 0;
+      if (kDB && blockIdx.x < nt) stage(blockIdx.x, 0);
+      cp_async_commit();
+      for (int t = blockIdx.x; t < nt; t += nb) {
+        if constexpr (kDB) {
+          if (t + nb < nt) stage(t + nb, buf ^ 1);
+          cp_async_commit();
+          cp_async_wait<1>();
+        } else {
+          stage(t, 0);
+          cp_async_commit();
+          cp_async_wait<0>();
+        }
         __syncthreads();
+        const double* P = smem + buf * G::kSb;
+        const double* Wt = P + G::NP * D;
+        const double* Rq = Wt + G::S * G::NPW;
+        const double* Bo = Rq + G::NV * D;
+        const TileIdx ti = tile_of<R, D>(g, t);
         for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
           bad |= !isfinite(P[hpos * D + c]);
-          double acc = 0.0;
-#pragma unroll
-          for (int e = 0; e < 2 * G::S; ++e) {
-            const bool fwd = e >= G::S;
-            const int s = fwd ? e - G::S : G::S - 1 - e;
-            const int npos = fwd ? hpos + T::dy(s) * G::HW + T::dx(s) : hpos - T::dy(s) * G::HW - T::dx(s);
-            const int opos = fwd ? hpos : npos;
-            const int jpos = fwd ? npos : hpos;
-            const double w = Wt[s * G::NP + opos];
-            if (w == 0.0) continue;
-            const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
-            double bo = 0.0;
-            if (b_old) {
-              if constexpr (G::kStageB)
-                bo = Bo[(s * G::NO + opos) * D + c];
-              else
-                bo = __ldcg(b_old + slot * D + c);
-            }
-            const double nw = -w;
-            const double my = w * P[opos * D + c] + nw * P[jpos * D + c];
-            const double sh = shrink1(my + bo, a.gamma);
-            const double bn = bo + (my - sh);
-            acc += (fwd ? w : nw) * (sh - bn);
-            if (fwd) {
-              b_new[slot * D + c] = bn;
-              if (s_out) s_out[slot * D + c] = sh;
-            }
-          }
+          const double acc = tile_sb_element<D, R, false>(g, P, Wt, Bo, b_old, b_new, s_out, a.gamma, hpos, c, v,
+                                                       ti.y0 + hpos / G::HW - R);
           if (rhs_out) rhs_out[v * D + c] = a.hl * acc + Rq[tv * D + c];
         });
         __syncthreads();
+        if constexpr (kDB) buf ^= 1;
       }
+      cp_async_wait<0>();
     }
     ebcur ^= 1;
     b_zero = false;

@@ -271,6 +271,7 @@ struct pfe_solver {
   Ctl* h_ctl = nullptr;  // pinned mirror
   double* partials = nullptr;    // init / update partials (and objective, norms)
   double* partials_b = nullptr;  // spmv partials
+  double* totals = nullptr;      // PCG grid totals written by the producers' last block [4][kMaxD]
   double* partials_c = nullptr;  // init partials of the resident persistent kernel (two sets)
   int max_grid = 0;
   double* rbuf = nullptr;
@@ -362,6 +363,17 @@ struct pfe_state {
 namespace {
 
 // ------------------------------------------------------------- set-up -----
+
+// Off-diagonal entries of A per forward stencil slot, exactly as
+// form_normal_matrix forms them ((hl * (+w)) * (-w) == -((hl * w) * w),
+// sparse.cpp:114); +0.0 marks an absent edge (Grid::cf).
+__global__ void k_grid_coef(long cnt, const double* __restrict__ wf, double hl, double* __restrict__ cf) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < cnt;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double w = wf[i];
+    cf[i] = w != 0.0 ? -((hl * w) * w) : 0.0;
+  }
+}
 
 struct HostGraph {
   int n;
@@ -477,6 +489,14 @@ Incidence build_incidence(const HostGraph& g) {
 // Builds the device topology.  Diagonal of A: sum over incident edges in
 // edge order of (hl * w) * w, then + (0.5 r) deg_v last — the accumulation
 // order csr_from_triplets applies to form_normal_matrix's triplets.
+double* grid_coef(pfe_solver* S, const double* dwf, long cnt, double hl, cudaStream_t st) {
+  double* dcf = S->mem.alloc<double>(static_cast<size_t>(cnt));
+  const int grid = static_cast<int>(std::min<long>(4L * S->sm * 8, (cnt + 255) / 256));
+  if (cnt > 0) k_grid_coef<<<std::max(1, grid), 256, 0, st>>>(cnt, dwf, hl, dcf);
+  CK(cudaGetLastError());
+  return dcf;
+}
+
 void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad) {
   const int n = g.n;
   const long m = g.m;
@@ -567,12 +587,15 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     double* dwf = S->mem.upload(wf, st);
     S->edge_row = std::move(slot_of);
     S->edge_rows = static_cast<long>(n) * S_;
+    double* dcf = grid_coef(S, dwf, static_cast<long>(n) * S_, hl, st);
     if (grad == 1) {
       S->topo.kind = pfe_host::kTopoGrid1;
       S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+      S->topo.g1.cf = dcf;
     } else {
       S->topo.kind = pfe_host::kTopoGrid2;
       S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+      S->topo.g2.cf = dcf;
     }
     return;
   }
@@ -698,6 +721,7 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   S->max_grid = S->sm * std::max(8, S->tab->max_blocks_per_sm());
   S->partials = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * 3 * pfe_dev::kMaxD);
   S->partials_b = S->mem.alloc<double>(static_cast<size_t>(S->max_grid) * pfe_dev::kMaxD);
+  S->totals = S->mem.alloc<double>(4 * pfe_dev::kMaxD);
   S->partials_c = S->mem.alloc<double>(static_cast<size_t>(S->sm) * 6 * pfe_dev::kMaxD);
   S->ctl = S->mem.alloc<Ctl>(1);
   CK(cudaMemsetAsync(S->ctl, 0, sizeof(Ctl), S->stream));
@@ -868,6 +892,19 @@ PcgArgs pcg_args(pfe_state* st, const double* rhs) {
   a.rd_b = S->partials_b;
   a.rank_major = 0;
   S->tab->pcg_grids(S->topo, S->lv(), &a.nb_init, &a.nb_spmv, &a.nb_update);
+  // Large general graphs: producers reduce their own partials (last block)
+  // and the consumers read the totals (their gather-bound kernels cannot hide
+  // an nb^2 consumer-side reduction).  Grids and small systems keep the
+  // consumer-side reduction, which overlaps the consumer's first loads and
+  // has no serial tail.
+  a.tot_a = S->totals;
+  a.tot_b = S->totals + 3 * pfe_dev::kMaxD;
+  a.totals = S->topo.kind == pfe_host::kTopoCsr && static_cast<long>(S->n) * S->d >= (1L << 22);
+  if (a.totals) {
+    a.rd_a = a.tot_a;
+    a.rd_b = a.tot_b;
+    a.nb_init = a.nb_spmv = a.nb_update = 1;
+  }
   a.tol = S->prm.pcg_rel_tol;
   a.max_iter = S->prm.pcg_max_iter;
   a.use_cond = 0;

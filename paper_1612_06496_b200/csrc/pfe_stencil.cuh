@@ -46,6 +46,10 @@ struct TileGeo {
   // block per SM), so they get 16 warps to keep enough loads in flight
   static constexpr int NT = R == 2 ? 512 : 256;
   static constexpr int HW = TW + 2 * R, HH = TH + 2 * R, NP = HW * HH;
+  // pitch of the slot-planar weight / coefficient planes: odd, so the 8-byte
+  // cp.async writes of the S slots of one position (consecutive lanes) land
+  // in different banks (an even pitch that is a multiple of 16 puts all S in one)
+  static constexpr int NPW = NP + 1;
   static constexpr int S = GridTopo<R>::S;
   static constexpr int NO = (TH + R) * HW;  // positions owning edges that touch the tile
   static constexpr bool kStageB = (R == 1);
@@ -53,10 +57,10 @@ struct TileGeo {
   static constexpr bool kEl = (32 % D == 0);
   static constexpr int V = kEl ? 1 : D;  // columns accumulated per thread
   // shared-memory footprints (doubles); every array offset stays 16-byte aligned
-  static constexpr int kInit = NP * D + S * NP + NV * D + 2 * NV;
-  static constexpr int kSpmv = 2 * NP * D + NP + S * NP + NV;
-  static constexpr int kSb = NP * D + S * NP + NV * D + (kStageB ? S * NO * D : 0);
-  static_assert(NP % 2 == 0 && NO % 2 == 0, "alignment of staged arrays");
+  static constexpr int kInit = NP * D + S * NPW + NV * D + 2 * NV;
+  static constexpr int kSpmv = 2 * NP * D + NP + S * NPW + NV;
+  static constexpr int kSb = NP * D + S * NPW + NV * D + (kStageB ? S * NO * D : 0);
+  static_assert(NP % 2 == 0 && NO % 2 == 0 && (S * NPW) % 2 == 0, "alignment of staged arrays");
 };
 
 struct TileIdx {
@@ -102,15 +106,15 @@ __device__ __forceinline__ void stage_rows(const Grid<R>& g, TileIdx ti, const d
 }
 
 // Slot-major planes: src [n][S][W] -> dst[s][pos][W] for halo rows [0, nrows)
-// (npos = nrows * HW positions per plane).
+// (nrows * HW positions per plane, planes `pitch` positions apart).
 template <int R, int D, int S, int W>
 __device__ __forceinline__ void stage_planes(const Grid<R>& g, TileIdx ti, const double* __restrict__ src, double* dst,
-                                             int nrows) {
+                                             int nrows, int pitch) {
   using G = TileGeo<R, D>;
   constexpr int CH = (W % 2 == 0) ? 2 : 1;
   constexpr int PER = W / CH;
-  const int npos = nrows * G::HW;
-  const int total = npos * S * PER;
+  const int npos = pitch;
+  const int total = nrows * G::HW * S * PER;
   for (int c = threadIdx.x; c < total; c += G::NT) {
     const int pos = c / (S * PER);
     const int rem = c - pos * (S * PER);
@@ -164,33 +168,35 @@ __device__ __forceinline__ void for_tile_elements(const Grid<R>& g, TileIdx ti, 
 }
 
 // (A p)_v, column c, in ascending column order (sparse.cpp:77-83): backward
-// slots, diagonal, forward slots.  Wt is slot-planar [S][NP].
+// slots, diagonal, forward slots.  Ct is slot-planar [S][NPW] and holds the
+// off-diagonal entries -((hl w) w) (Grid::cf, sparse.cpp:114), +0.0 for an
+// absent edge: a present edge's entry always has its sign bit set (it is
+// negative, or -0.0 if hl w^2 underflows), so the sign bit is the presence test.
 template <int D, int R>
-__device__ __forceinline__ double tile_apply_A(double hl, const double* P, const double* Wt, int hpos, int c,
-                                               double diag_v) {
+__device__ __forceinline__ double tile_apply_A(const double* P, const double* Ct, int hpos, int c, double diag_v) {
   using G = TileGeo<R, D>;
   using T = GridTopo<R>;
-  // branch-free: every term is loaded and formed, absent edges (w == 0) are
-  // skipped by a select, so all loads are in flight before the serial
-  // reference-order additions
+  // branch-free: every term is loaded and formed, absent edges are skipped by
+  // a select, so all loads are in flight before the serial reference-order
+  // additions
   double t[2 * G::S + 1];
   bool nz[2 * G::S + 1];
 #pragma unroll
   for (int j = 0; j < G::S; ++j) {
     const int s = G::S - 1 - j;
     const int npos = hpos - T::dy(s) * G::HW - T::dx(s);
-    const double w = Wt[s * G::NP + npos];
-    nz[j] = w != 0.0;
-    t[j] = -((hl * w) * w) * P[npos * D + c];
+    const double cw = Ct[s * G::NPW + npos];
+    nz[j] = __double_as_longlong(cw) < 0;
+    t[j] = cw * P[npos * D + c];
   }
   nz[G::S] = true;
   t[G::S] = diag_v * P[hpos * D + c];
 #pragma unroll
   for (int s = 0; s < G::S; ++s) {
     const int npos = hpos + T::dy(s) * G::HW + T::dx(s);
-    const double w = Wt[s * G::NP + hpos];
-    nz[G::S + 1 + s] = w != 0.0;
-    t[G::S + 1 + s] = -((hl * w) * w) * P[npos * D + c];
+    const double cw = Ct[s * G::NPW + hpos];
+    nz[G::S + 1 + s] = __double_as_longlong(cw) < 0;
+    t[G::S + 1 + s] = cw * P[npos * D + c];
   }
   double q = 0.0;
 #pragma unroll
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
   extern __shared__ double smem[];
   double* P = smem;                  // x0 halo [NP][D]
   double* Wt = P + G::NP * D;        // [S][NP]
-  double* Bv = Wt + G::S * G::NP;    // rhs interior [NV][D]
+  double* Bv = Wt + G::S * G::NPW;    // rhs interior [NV][D]
   double* Dg = Bv + G::NV * D;       // diag interior [NV]
   double* Iv = Dg + G::NV;           // inv diag interior [NV]
   double acc[3][V] = {};
@@ -214,14 +220,14 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
   for (int t = blockIdx.x; t < nt; t += gridDim.x) {
     const TileIdx ti = tile_of<R, D>(g, t);
     stage_rows<R, D, D>(g, ti, a.x0, P, G::HH);
-    stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+    stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
     stage_interior<R, D, D>(g, ti, a.rhs, Bv);
     stage_interior<R, D, 1>(g, ti, g.diag, Dg);
     stage_interior<R, D, 1>(g, ti, g.invd, Iv);
     cp_async_wait_all();
     __syncthreads();
     for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-      const double ax = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
+      const double ax = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
       const double b = Bv[tv * D + c];
       const double r = b - ax;
       const double z = Iv[tv] * r;
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
     });
     __syncthreads();
   }
-  block_reduce_store<3, D, V, G::NT>(acc, a.part_a);  // reduced by the first SpMV
+  store_partials<3, D, V, G::NT>(a, acc, a.part_a, a.tot_a);  // reduced by the first SpMV
 }
 
 // ---------------------------------------------------------------- spmv ----
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
   double* Rs = P + G::NP * D;        // r halo [NP][D]
   double* Iv = Rs + G::NP * D;       // inv diag halo [NP]
   double* Wt = Iv + G::NP;           // [S][NP]
-  double* Dg = Wt + G::S * G::NP;    // diag interior [NV]
+  double* Dg = Wt + G::S * G::NPW;    // diag interior [NV]
   __shared__ ColView<D> cv;
   const bool first = a.phase == 0;
   double* pnew = pcg_pnew(a);
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
       stage_rows<R, D, D>(g, ti, a.r, Rs, G::HH);
       stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
     }
-    stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+    stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
     stage_interior<R, D, 1>(g, ti, g.diag, Dg);
     if (!checked) {  // stop test + beta while the copies are in flight
       if (!spmv_prologue<D, G::NT>(a, cv)) {
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
       __syncthreads();
     }
     for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-      const double q = tile_apply_A<D, R>(g.hl, P, Wt, hpos, c, Dg[tv]);
+      const double q = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
       const double pv = P[hpos * D + c];
       a.q[v * D + c] = q;
       if (!first) pnew[v * D + c] = pv;
@@ -291,15 +297,69 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
     __syncthreads();
   }
   if (!checked && !spmv_prologue<D, G::NT>(a, cv)) return;  // block without tiles
-  block_reduce_store<1, D, V, G::NT>(acc, a.part_b);  // reduced by the update
+  store_partials<1, D, V, G::NT>(a, acc, a.part_b, a.tot_b);  // reduced by the update
 }
 
 // ----------------------------------------------------- split-Bregman pass -
-// Per interior vertex v and column: incident edges in edge order (backward
-// slots S-1..0 owned by neighbours, then forward slots 0..S-1 owned by v),
-// each evaluated as solver.cpp:96-98 and accumulated into the next rhs
-// (solver.cpp:83-84).  8-neighbour grids stage b_old of all those edges
-// (slot-planar); 5x5 grids read it from global memory.
+// One (vertex, column) element of the pass from a staged tile: every incident
+// edge in edge order (backward slots S-1..0, owned by neighbours, then forward
+// slots 0..S-1, owned by v) evaluated as solver.cpp:96-98; returns
+// sum_e M_ev (s_e - b_e') for the next rhs (solver.cpp:83-84).  The owner
+// stores b' (and s); in a row band, edges owned by the halo rows above are
+// replicas this band updates identically (vy = image row of v).  b_old comes from the staged
+// owner planes Bo (8-neighbour grids) or from global memory, in which case
+// all 2S loads are issued before the first use (one round trip, not 2S).
+template <int D, int R, bool kNc>
+__device__ __forceinline__ double tile_sb_element(const Grid<R>& g, const double* P, const double* Wt, const double* Bo,
+                                                  const double* __restrict__ b_old, double* b_new, double* s_out,
+                                                  double gamma, int hpos, int c, long v, int vy) {
+  using G = TileGeo<R, D>;
+  using T = GridTopo<R>;
+  double bo[2 * G::S];
+#pragma unroll
+  for (int e = 0; e < 2 * G::S; ++e) {
+    const bool fwd = e >= G::S;
+    const int s = fwd ? e - G::S : G::S - 1 - e;
+    const int opos = fwd ? hpos : hpos - T::dy(s) * G::HW - T::dx(s);
+    bo[e] = 0.0;
+    if (b_old && Wt[s * G::NPW + opos] != 0.0) {
+      if constexpr (G::kStageB) {
+        bo[e] = Bo[(s * G::NO + opos) * D + c];
+      } else {
+        const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
+        // kNc: b_old is read-only for this launch (multi-kernel path: the
+        // non-coherent path); else it was written earlier in the same
+        // persistent launch, before a grid barrier: a plain (coherent) load,
+        // still L1-cached so the other endpoint's read of the edge can hit
+        bo[e] = kNc ? __ldg(b_old + slot * D + c) : b_old[slot * D + c];
+      }
+    }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < 2 * G::S; ++e) {
+    const bool fwd = e >= G::S;
+    const int s = fwd ? e - G::S : G::S - 1 - e;
+    const int npos = fwd ? hpos + T::dy(s) * G::HW + T::dx(s) : hpos - T::dy(s) * G::HW - T::dx(s);
+    const int opos = fwd ? hpos : npos;  // owner = first endpoint i
+    const int jpos = fwd ? npos : hpos;
+    const double w = Wt[s * G::NPW + opos];
+    if (w == 0.0) continue;
+    const double nw = -w;
+    const double my = w * P[opos * D + c] + nw * P[jpos * D + c];
+    const double sh = shrink1(my + bo[e], gamma);
+    const double bn = bo[e] + (my - sh);
+    acc += (fwd ? w : nw) * (sh - bn);
+    if (fwd || vy - T::dy(s) < g.row_lo) {
+      const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
+      b_new[slot * D + c] = bn;
+      if (s_out) s_out[slot * D + c] = sh;
+    }
+  }
+  return acc;
+}
+
+// The pass over a tile grid (tile_sb_element per element).
 template <int D, int R>
 __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, SbArgs a) {
   using G = TileGeo<R, D>;
@@ -307,52 +367,24 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, S
   extern __shared__ double smem[];
   double* P = smem;                 // Y halo [NP][D]
   double* Wt = P + G::NP * D;       // [S][NP]
-  double* Rq = Wt + G::S * G::NP;   // rq interior [NV][D]
+  double* Rq = Wt + G::S * G::NPW;   // rq interior [NV][D]
   double* Bo = Rq + G::NV * D;      // b_old of owners [S][NO][D] (8-nbr only)
   const int nt = num_tiles<R, D>(g);
   int bad = 0;
   for (int t = blockIdx.x; t < nt; t += gridDim.x) {
     const TileIdx ti = tile_of<R, D>(g, t);
     stage_rows<R, D, D>(g, ti, a.y, P, G::HH);
-    stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH);
+    stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH, G::NPW);
     if (a.rhs) stage_interior<R, D, D>(g, ti, a.rq, Rq);
     if constexpr (G::kStageB) {
-      if (a.b_old) stage_planes<R, D, G::S, D>(g, ti, a.b_old, Bo, G::TH + R);
+      if (a.b_old) stage_planes<R, D, G::S, D>(g, ti, a.b_old, Bo, G::TH + R, G::NO);
     }
     cp_async_wait_all();
     __syncthreads();
     for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
       bad |= !isfinite(P[hpos * D + c]);
-      double acc = 0.0;
-#pragma unroll
-      for (int e = 0; e < 2 * G::S; ++e) {
-        const bool fwd = e >= G::S;
-        const int s = fwd ? e - G::S : G::S - 1 - e;
-        const int npos = fwd ? hpos + T::dy(s) * G::HW + T::dx(s) : hpos - T::dy(s) * G::HW - T::dx(s);
-        const int opos = fwd ? hpos : npos;  // owner = first endpoint i
-        const int jpos = fwd ? npos : hpos;
-        const double w = Wt[s * G::NP + opos];
-        if (w == 0.0) continue;
-        const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
-        double bo = 0.0;
-        if (a.b_old) {
-          if constexpr (G::kStageB)
-            bo = Bo[(s * G::NO + opos) * D + c];
-          else
-            bo = __ldg(a.b_old + slot * D + c);
-        }
-        const double nw = -w;
-        const double my = w * P[opos * D + c] + nw * P[jpos * D + c];
-        const double sh = shrink1(my + bo, a.gamma);
-        const double bn = bo + (my - sh);
-        acc += (fwd ? w : nw) * (sh - bn);
-        // the owner stores b (and s); in a row band, edges owned by the halo
-        // rows above are replicas that this band updates identically
-        if (fwd || static_cast<int>(v / g.W) - T::dy(s) < g.row_lo) {
-          a.b_new[slot * D + c] = bn;
-          if (a.s_out) a.s_out[slot * D + c] = sh;
-        }
-      }
+      const double acc = tile_sb_element<D, R, true>(g, P, Wt, Bo, a.b_old, a.b_new, a.s_out, a.gamma, hpos, c, v,
+                                                          ti.y0 + hpos / G::HW - R);
       if (a.rhs) a.rhs[v * D + c] = a.hl * acc + Rq[tv * D + c];
     });
     __syncthreads();
