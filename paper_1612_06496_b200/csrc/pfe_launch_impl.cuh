@@ -1,7 +1,10 @@
 // Template bodies of the launch table (included by pfe_kernels_d*.cu only).
 #pragma once
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -23,6 +26,61 @@ inline void check_launch(const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
 }
 #define PFE_LAUNCHED(name) check_launch(name)
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda).
+inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Map of an image-row array [H][W][K] (fp64) with box (K, bw, bh); K == 1
+// arrays are 2-D.  Fails (false) when TMA's alignment rules are not met.
+inline bool encode_rows(CUtensorMap* m, const void* base, int K, int W, int H, int bw, int bh) {
+  auto enc = tma_encoder();
+  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r;
+  if (K == 1) {
+    if ((W * 8) % 16 != 0 || (bw * 8) % 16 != 0) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(W) * 8};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh)};
+    r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    if ((K * 8) % 16 != 0 || K > 256) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 8, static_cast<cuuint64_t>(W) * K * 8};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(K), static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh)};
+    r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS;
+}
+
+// Phases of the persistent kernel that stage with TMA (PersistArgs::tma
+// bits; 16: also the one-wide arrays diag / inv diag).  Default: every phase
+// for 5x5 grids; 8-neighbour grids keep cp.async (their TMA staging faults
+// with an illegal-instruction error on B200 that is not understood yet, see
+// DESIGN.md).  PFE_TMA=0 forces cp.async everywhere (A/B tests), PFE_TMA=1
+// every phase, PFE_TMA=<mask> selects phases.
+inline int tma_mask(int radius) {
+  const char* e = std::getenv("PFE_TMA");
+  if (!e || !e[0]) return radius == 2 ? 31 : 0;
+  return std::atoi(e) == 1 ? 31 : std::atoi(e);
+}
 
 template <int D>
 struct Impl {
@@ -257,7 +315,33 @@ struct Impl {
         return 2;
       }
     }
-    const int grid = per_sm * l.sm;
+    // TMA staging: every tile array is a box of one tensor map (even d and
+    // image width; pfe_tma.cuh)
+    using G = TileGeo<R, D>;
+    a.tma = 0;
+    if (tma_mask(R) != 0 && D % 2 == 0 && g.W % 2 == 0) {
+      TileMaps& tm = a.tm;
+      const int W = g.W, H = g.H;
+      bool ok = true;
+      for (int i = 0; i < 2; ++i) {
+        ok = ok && encode_rows(&tm.y[i], in.ybuf[i], D, W, H, G::HW, G::HH);
+        ok = ok && encode_rows(&tm.p[i], in.pbuf[i], D, W, H, G::HW, G::HH);
+      }
+      ok = ok && encode_rows(&tm.r_halo, in.r, D, W, H, G::HW, G::HH);
+      ok = ok && encode_rows(&tm.r_int, in.r, D, W, H, G::TW, G::TH);
+      ok = ok && encode_rows(&tm.rhs0_int, in.rhs0, D, W, H, G::TW, G::TH);
+      ok = ok && encode_rows(&tm.iv_halo, g.invd, 1, W, H, G::HW, G::HH);
+      ok = ok && encode_rows(&tm.iv_int, g.invd, 1, W, H, G::TW, G::TH);
+      ok = ok && encode_rows(&tm.dg_int, g.diag, 1, W, H, G::TW, G::TH);
+      ok = ok && encode_rows(&tm.cf_halo, g.cf, G::S, W, H, G::HW, G::HH);
+      ok = ok && encode_rows(&tm.wf_halo, g.wf, G::S, W, H, G::HW, G::HH);
+      if (in.rq) ok = ok && encode_rows(&tm.rq_int, in.rq, D, W, H, G::TW, G::TH);
+      if (G::kStageB)
+        for (int i = 0; i < 2; ++i) ok = ok && encode_rows(&tm.bo[i], in.eb[i], G::S * D, W, H, G::HW, G::TH + R);
+      a.tma = ok ? tma_mask(R) : 0;
+    }
+    const char* one = std::getenv("PFE_PERSIST_ONE_CTA");  // debugging: one block per SM
+    const int grid = (one && one[0] == '1' ? 1 : per_sm) * l.sm;
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_sb_persistent<D, R>),
                                                       dim3(grid), dim3(TileGeo<R, D>::NT), args, smem, l.stream);
     if (e != cudaSuccess)

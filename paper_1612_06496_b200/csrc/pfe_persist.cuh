@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include "pfe_stencil.cuh"
+#include "pfe_tma.cuh"
 
 namespace pfe_dev {
 
@@ -67,6 +68,10 @@ struct PersistArgs {
   double* part_c;    // init partials, two buffers alternating by inner iteration
   int rgx, rgy;      // region grid: blocks = rgx * rgy, block b owns region (b / rgx, b % rgx)
   int rhw, rnp;      // smem pitch (max region width + 2R) and positions per plane
+  // tiled persistent kernel: phases staging their tiles with TMA (bit 0
+  // init, 1 SpMV, 2 split-Bregman pass, 3 b_old owner rows) or cp.async
+  int tma;
+  TileMaps tm;
 };
 
 // Per-block column state (identical in every block).
@@ -94,12 +99,13 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int D, int R>
-__global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persistent(PersistArgs<R> a) {
+__global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
+    k_sb_persistent(const __grid_constant__ PersistArgs<R> a) {
   using G = TileGeo<R, D>;
   using T = GridTopo<R>;
   constexpr int V = G::V;
   constexpr int NT = G::NT;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(1024) double smem[];  // 1024: TMA box destinations
   __shared__ PersistCols<D> pc;
   __shared__ double tot[3][D];
   __shared__ double tot1[1][D];
@@ -112,6 +118,28 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
   int bad = 0;
   int trace_n = 0;
   PFE_TRACE(0);
+  // TMA staging: one mbarrier per tile buffer; tph holds each buffer's
+  // expected phase parity (identical in every thread)
+  __shared__ alignas(8) uint64_t tbar[2];
+  const bool tma_any = a.tma != 0;
+  uint32_t tph = 0;
+  if (tma_any && threadIdx.x == 0) {
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto tile_wait = [&](bool tma, int buf, bool more) {
+    if (tma) {
+      mbar_wait(&tbar[buf], (tph >> buf) & 1u);
+      tph ^= 1u << buf;
+    }
+    if (more)
+      cp_async_wait<1>();
+    else
+      cp_async_wait<0>();
+  };
+  constexpr uint32_t kHalo = G::NP * 8, kInt = G::NV * 8;
 
   for (int inner = 0; inner < a.n_inner; ++inner) {
     const bool last = inner == a.n_inner - 1;
@@ -122,15 +150,34 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
     // ---------------- PCG init: r = b - A x0, p = D^-1 r (pcg.cpp:49-66)
     {
       double acc[3][V] = {};
+      const bool tma = (a.tma & 1) != 0, tma1 = (a.tma & 16) != 0;
       auto stage = [&](int t, int buf) {
         double* P = smem + buf * G::kInit;
-        double* Wt = P + G::NP * D;
-        double* Bv = Wt + G::S * G::NPW;
-        double* Dg = Bv + G::NV * D;
-        double* Iv = Dg + G::NV;
+        double* Wt = P + G::kI_W;
+        double* Bv = P + G::kI_B;
+        double* Dg = P + G::kI_Dg;
+        double* Iv = P + G::kI_Iv;
         const TileIdx ti = tile_of<R, D>(g, t);
+        if (tma) {
+          if (threadIdx.x == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&tbar[buf], kHalo * (D + G::S) + kInt * (D + (tma1 ? 2 : 0)));
+            tma_rows<D>(P, &a.tm.y[ycur], ti.x0 - R, ti.y0 - R, &tbar[buf]);
+            tma_rows<G::S>(Wt, &a.tm.cf_halo, ti.x0 - R, ti.y0 - R, &tbar[buf]);
+            tma_rows<D>(Bv, inner == 0 ? &a.tm.rhs0_int : &a.tm.r_int, ti.x0, ti.y0, &tbar[buf]);
+            if (tma1) {
+              tma_rows<1>(Dg, &a.tm.dg_int, ti.x0, ti.y0, &tbar[buf]);
+              tma_rows<1>(Iv, &a.tm.iv_int, ti.x0, ti.y0, &tbar[buf]);
+            }
+          }
+          if (!tma1) {
+            stage_interior<R, D, 1>(g, ti, g.diag, Dg);
+            stage_interior<R, D, 1>(g, ti, g.invd, Iv);
+          }
+          return;
+        }
         stage_rows<R, D, D>(g, ti, x0, P, G::HH);
-        stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
+        stage_rows<R, D, G::S>(g, ti, g.cf, Wt, G::HH);
         stage_interior<R, D, D>(g, ti, rhs, Bv);
         stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         stage_interior<R, D, 1>(g, ti, g.invd, Iv);
@@ -141,13 +188,13 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
       for (int t = blockIdx.x; t < nt; t += nb) {
         if (t + nb < nt) stage(t + nb, buf ^ 1);
         cp_async_commit();
-        cp_async_wait<1>();
+        tile_wait(tma, buf, true);
         __syncthreads();
         const double* P = smem + buf * G::kInit;
-        const double* Wt = P + G::NP * D;
-        const double* Bv = Wt + G::S * G::NPW;
-        const double* Dg = Bv + G::NV * D;
-        const double* Iv = Dg + G::NV;
+        const double* Wt = P + G::kI_W;
+        const double* Bv = P + G::kI_B;
+        const double* Dg = P + G::kI_Dg;
+        const double* Iv = P + G::kI_Iv;
         const TileIdx ti = tile_of<R, D>(g, t);
         for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
           const double ax = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
@@ -206,19 +253,39 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
       // SpMV with the fused direction update p = z + beta p
       {
         double acc[1][V] = {};
+        const bool tma = (a.tma & 2) != 0, tma1 = (a.tma & 16) != 0;
         auto stage = [&](int t, int buf) {
           double* P = smem + buf * G::kSpmv;
-          double* Rs = P + G::NP * D;
-          double* Iv = Rs + G::NP * D;
-          double* Wt = Iv + G::NP;
-          double* Dg = Wt + G::S * G::NPW;
+          double* Rs = P + G::kS_Rs;
+          double* Iv = P + G::kS_Iv;
+          double* Wt = P + G::kS_W;
+          double* Dg = P + G::kS_Dg;
           const TileIdx ti = tile_of<R, D>(g, t);
+          if (tma) {
+            if (threadIdx.x == 0) {
+              fence_proxy_async();
+              mbar_expect_tx(&tbar[buf], kHalo * (D + G::S) + (tma1 ? kInt : 0u) +
+                                             (first ? 0u : kHalo * (D + (tma1 ? 1 : 0))));
+              tma_rows<D>(P, &a.tm.p[pold == a.pbuf[1] ? 1 : 0], ti.x0 - R, ti.y0 - R, &tbar[buf]);
+              if (!first) {
+                tma_rows<D>(Rs, &a.tm.r_halo, ti.x0 - R, ti.y0 - R, &tbar[buf]);
+                if (tma1) tma_rows<1>(Iv, &a.tm.iv_halo, ti.x0 - R, ti.y0 - R, &tbar[buf]);
+              }
+              tma_rows<G::S>(Wt, &a.tm.cf_halo, ti.x0 - R, ti.y0 - R, &tbar[buf]);
+              if (tma1) tma_rows<1>(Dg, &a.tm.dg_int, ti.x0, ti.y0, &tbar[buf]);
+            }
+            if (!tma1) {
+              if (!first) stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
+              stage_interior<R, D, 1>(g, ti, g.diag, Dg);
+            }
+            return;
+          }
           stage_rows<R, D, D>(g, ti, pold, P, G::HH);
           if (!first) {
             stage_rows<R, D, D>(g, ti, a.r, Rs, G::HH);
             stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
           }
-          stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
+          stage_rows<R, D, G::S>(g, ti, g.cf, Wt, G::HH);
           stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         };
         int buf = 0;
@@ -227,13 +294,13 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
         for (int t = blockIdx.x; t < nt; t += nb) {
           if (t + nb < nt) stage(t + nb, buf ^ 1);
           cp_async_commit();
-          cp_async_wait<1>();
+          tile_wait(tma, buf, true);
           __syncthreads();
           double* P = smem + buf * G::kSpmv;
-          const double* Rs = P + G::NP * D;
-          const double* Iv = Rs + G::NP * D;
-          const double* Wt = Iv + G::NP;
-          const double* Dg = Wt + G::S * G::NPW;
+          const double* Rs = P + G::kS_Rs;
+          const double* Iv = P + G::kS_Iv;
+          const double* Wt = P + G::kS_W;
+          const double* Dg = P + G::kS_Dg;
           if (!first) {
             for (int e = threadIdx.x; e < G::NP * D; e += NT) {
               const int pos = e / D, c = e - pos * D;
@@ -249,6 +316,9 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
             if (!first) pnew[v * D + c] = pv;
             acc[0][k] += pv * qv;
           });
+          // p' was formed in place (generic proxy); a later TMA copy into
+          // this buffer (async proxy) must be ordered after those writes
+          if (tma) fence_proxy_async();
           __syncthreads();
           buf ^= 1;
         }
@@ -408,17 +478,36 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
       // buffer); 5x5 grids read b_old from global memory and double-buffer
       // the tile staging like the SpMV
       constexpr bool kDB = !G::kStageB;
+      const bool tma = (a.tma & 4) != 0, tma_b = (a.tma & 8) != 0;
       auto stage = [&](int t, int buf) {
         double* P = smem + buf * G::kSb;
-        double* Wt = P + G::NP * D;
-        double* Rq = Wt + G::S * G::NPW;
-        double* Bo = Rq + G::NV * D;
+        double* Wt = P + G::kB_W;
+        double* Rq = P + G::kB_Rq;
+        double* Bo = P + G::kB_Bo;
         const TileIdx ti = tile_of<R, D>(g, t);
+        if (tma) {
+          if (threadIdx.x == 0) {
+            fence_proxy_async();
+            const bool stage_b = G::kStageB && b_old && tma_b;
+            mbar_expect_tx(&tbar[buf], kHalo * (D + G::S) + (rhs_out ? kInt * D : 0u) +
+                                           (stage_b ? static_cast<uint32_t>(G::NO * G::S * D * 8) : 0u));
+            tma_rows<D>(P, &a.tm.y[ycur], ti.x0 - R, ti.y0 - R, &tbar[buf]);
+            tma_rows<G::S>(Wt, &a.tm.wf_halo, ti.x0 - R, ti.y0 - R, &tbar[buf]);
+            if (rhs_out) tma_rows<D>(Rq, &a.tm.rq_int, ti.x0, ti.y0, &tbar[buf]);
+            if constexpr (G::kStageB) {
+              if (stage_b) tma_rows<G::S * D>(Bo, &a.tm.bo[ebcur], ti.x0 - R, ti.y0 - R, &tbar[buf]);
+            }
+          }
+          if constexpr (G::kStageB) {
+            if (b_old && !tma_b) stage_rows<R, D, G::S * D>(g, ti, b_old, Bo, G::TH + R);
+          }
+          return;
+        }
         stage_rows<R, D, D>(g, ti, y, P, G::HH);
-        stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH, G::NPW);
+        stage_rows<R, D, G::S>(g, ti, g.wf, Wt, G::HH);
         if (rhs_out) stage_interior<R, D, D>(g, ti, a.rq, Rq);
         if constexpr (G::kStageB) {
-          if (b_old) stage_planes<R, D, G::S, D>(g, ti, b_old, Bo, G::TH + R, G::NO);
+          if (b_old) stage_rows<R, D, G::S * D>(g, ti, b_old, Bo, G::TH + R);
         }
       };
       int buf = 0;
@@ -428,17 +517,17 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2) k_sb_persis
         if constexpr (kDB) {
           if (t + nb < nt) stage(t + nb, buf ^ 1);
           cp_async_commit();
-          cp_async_wait<1>();
+          tile_wait(tma, buf, true);
         } else {
           stage(t, 0);
           cp_async_commit();
-          cp_async_wait<0>();
+          tile_wait(tma, 0, false);
         }
         __syncthreads();
         const double* P = smem + buf * G::kSb;
-        const double* Wt = P + G::NP * D;
-        const double* Rq = Wt + G::S * G::NPW;
-        const double* Bo = Rq + G::NV * D;
+        const double* Wt = P + G::kB_W;
+        const double* Rq = P + G::kB_Rq;
+        const double* Bo = P + G::kB_Bo;
         const TileIdx ti = tile_of<R, D>(g, t);
         for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
           bad |= !isfinite(P[hpos * D + c]);

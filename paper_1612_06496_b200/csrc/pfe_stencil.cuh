@@ -46,21 +46,26 @@ struct TileGeo {
   // block per SM), so they get 16 warps to keep enough loads in flight
   static constexpr int NT = R == 2 ? 512 : 256;
   static constexpr int HW = TW + 2 * R, HH = TH + 2 * R, NP = HW * HH;
-  // pitch of the slot-planar weight / coefficient planes: odd, so the 8-byte
-  // cp.async writes of the S slots of one position (consecutive lanes) land
-  // in different banks (an even pitch that is a multiple of 16 puts all S in one)
-  static constexpr int NPW = NP + 1;
   static constexpr int S = GridTopo<R>::S;
   static constexpr int NO = (TH + R) * HW;  // positions owning edges that touch the tile
   static constexpr bool kStageB = (R == 1);
   // element-parallel compute: thread owns column tid % D of successive vertices
   static constexpr bool kEl = (32 % D == 0);
   static constexpr int V = kEl ? 1 : D;  // columns accumulated per thread
-  // shared-memory footprints (doubles); every array offset stays 16-byte aligned
-  static constexpr int kInit = NP * D + S * NPW + NV * D + 2 * NV;
-  static constexpr int kSpmv = 2 * NP * D + NP + S * NPW + NV;
-  static constexpr int kSb = NP * D + S * NPW + NV * D + (kStageB ? S * NO * D : 0);
-  static_assert(NP % 2 == 0 && NO % 2 == 0 && (S * NPW) % 2 == 0, "alignment of staged arrays");
+  // Shared-memory layouts (offsets in doubles, every array 128-byte aligned
+  // so it can be a TMA destination).  Everything is position-major: rows
+  // [pos][D], weights / coefficients [pos][S], b_old [opos][S][D] -- the
+  // layout of the global arrays, so a halo box is one rectangular copy.
+  static constexpr int al(int x) { return (x + 15) / 16 * 16; }
+  // init: x0 halo, coefficient halo, rhs / diag / inv diag interior
+  static constexpr int kI_W = al(NP * D), kI_B = kI_W + al(NP * S), kI_Dg = kI_B + al(NV * D),
+                       kI_Iv = kI_Dg + al(NV), kInit = kI_Iv + al(NV);
+  // spmv: p_old halo, r halo, inv diag halo, coefficient halo, diag interior
+  static constexpr int kS_Rs = al(NP * D), kS_Iv = kS_Rs + al(NP * D), kS_W = kS_Iv + al(NP),
+                       kS_Dg = kS_W + al(NP * S), kSpmv = kS_Dg + al(NV);
+  // sb pass: Y halo, weight halo, rq interior, b_old of owners (8-nbr only)
+  static constexpr int kB_W = al(NP * D), kB_Rq = kB_W + al(NP * S), kB_Bo = kB_Rq + al(NV * D),
+                       kSb = kB_Bo + (kStageB ? al(NO * S * D) : 0);
 };
 
 struct TileIdx {
@@ -102,26 +107,6 @@ __device__ __forceinline__ void stage_rows(const Grid<R>& g, TileIdx ti, const d
     long u;
     const bool in = halo_in<R, D>(g, ti, pos, u);
     cp_async(dst + pos * W + k, in ? src + u * W + k : src, in, CH * 8);
-  }
-}
-
-// Slot-major planes: src [n][S][W] -> dst[s][pos][W] for halo rows [0, nrows)
-// (nrows * HW positions per plane, planes `pitch` positions apart).
-template <int R, int D, int S, int W>
-__device__ __forceinline__ void stage_planes(const Grid<R>& g, TileIdx ti, const double* __restrict__ src, double* dst,
-                                             int nrows, int pitch) {
-  using G = TileGeo<R, D>;
-  constexpr int CH = (W % 2 == 0) ? 2 : 1;
-  constexpr int PER = W / CH;
-  const int npos = pitch;
-  const int total = nrows * G::HW * S * PER;
-  for (int c = threadIdx.x; c < total; c += G::NT) {
-    const int pos = c / (S * PER);
-    const int rem = c - pos * (S * PER);
-    const int s = rem / PER, k = (rem - s * PER) * CH;
-    long u;
-    const bool in = halo_in<R, D>(g, ti, pos, u);
-    cp_async(dst + (s * npos + pos) * W + k, in ? src + (u * S + s) * W + k : src, in, CH * 8);
   }
 }
 
@@ -168,7 +153,7 @@ __device__ __forceinline__ void for_tile_elements(const Grid<R>& g, TileIdx ti, 
 }
 
 // (A p)_v, column c, in ascending column order (sparse.cpp:77-83): backward
-// slots, diagonal, forward slots.  Ct is slot-planar [S][NPW] and holds the
+// slots, diagonal, forward slots.  Ct is position-major [NP][S] and holds the
 // off-diagonal entries -((hl w) w) (Grid::cf, sparse.cpp:114), +0.0 for an
 // absent edge: a present edge's entry always has its sign bit set (it is
 // negative, or -0.0 if hl w^2 underflows), so the sign bit is the presence test.
@@ -185,7 +170,7 @@ __device__ __forceinline__ double tile_apply_A(const double* P, const double* Ct
   for (int j = 0; j < G::S; ++j) {
     const int s = G::S - 1 - j;
     const int npos = hpos - T::dy(s) * G::HW - T::dx(s);
-    const double cw = Ct[s * G::NPW + npos];
+    const double cw = Ct[npos * G::S + s];
     nz[j] = __double_as_longlong(cw) < 0;
     t[j] = cw * P[npos * D + c];
   }
@@ -194,7 +179,7 @@ __device__ __forceinline__ double tile_apply_A(const double* P, const double* Ct
 #pragma unroll
   for (int s = 0; s < G::S; ++s) {
     const int npos = hpos + T::dy(s) * G::HW + T::dx(s);
-    const double cw = Ct[s * G::NPW + hpos];
+    const double cw = Ct[hpos * G::S + s];
     nz[G::S + 1 + s] = __double_as_longlong(cw) < 0;
     t[G::S + 1 + s] = cw * P[npos * D + c];
   }
@@ -211,16 +196,16 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
   constexpr int V = G::V;
   extern __shared__ double smem[];
   double* P = smem;                  // x0 halo [NP][D]
-  double* Wt = P + G::NP * D;        // [S][NP]
-  double* Bv = Wt + G::S * G::NPW;    // rhs interior [NV][D]
-  double* Dg = Bv + G::NV * D;       // diag interior [NV]
-  double* Iv = Dg + G::NV;           // inv diag interior [NV]
+  double* Wt = smem + G::kI_W;       // coefficients [NP][S]
+  double* Bv = smem + G::kI_B;       // rhs interior [NV][D]
+  double* Dg = smem + G::kI_Dg;      // diag interior [NV]
+  double* Iv = smem + G::kI_Iv;      // inv diag interior [NV]
   double acc[3][V] = {};
   const int nt = num_tiles<R, D>(g);
   for (int t = blockIdx.x; t < nt; t += gridDim.x) {
     const TileIdx ti = tile_of<R, D>(g, t);
     stage_rows<R, D, D>(g, ti, a.x0, P, G::HH);
-    stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
+    stage_rows<R, D, G::S>(g, ti, g.cf, Wt, G::HH);
     stage_interior<R, D, D>(g, ti, a.rhs, Bv);
     stage_interior<R, D, 1>(g, ti, g.diag, Dg);
     stage_interior<R, D, 1>(g, ti, g.invd, Iv);
@@ -249,10 +234,10 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
   constexpr int V = G::V;
   extern __shared__ double smem[];
   double* P = smem;                  // p (phase 0) or p_old -> p' in place [NP][D]
-  double* Rs = P + G::NP * D;        // r halo [NP][D]
-  double* Iv = Rs + G::NP * D;       // inv diag halo [NP]
-  double* Wt = Iv + G::NP;           // [S][NP]
-  double* Dg = Wt + G::S * G::NPW;    // diag interior [NV]
+  double* Rs = smem + G::kS_Rs;      // r halo [NP][D]
+  double* Iv = smem + G::kS_Iv;      // inv diag halo [NP]
+  double* Wt = smem + G::kS_W;       // coefficients [NP][S]
+  double* Dg = smem + G::kS_Dg;      // diag interior [NV]
   __shared__ ColView<D> cv;
   const bool first = a.phase == 0;
   double* pnew = pcg_pnew(a);
@@ -267,7 +252,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
       stage_rows<R, D, D>(g, ti, a.r, Rs, G::HH);
       stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
     }
-    stage_planes<R, D, G::S, 1>(g, ti, g.cf, Wt, G::HH, G::NPW);
+    stage_rows<R, D, G::S>(g, ti, g.cf, Wt, G::HH);
     stage_interior<R, D, 1>(g, ti, g.diag, Dg);
     if (!checked) {  // stop test + beta while the copies are in flight
       if (!spmv_prologue<D, G::NT>(a, cv)) {
@@ -322,9 +307,9 @@ __device__ __forceinline__ double tile_sb_element(const Grid<R>& g, const double
     const int s = fwd ? e - G::S : G::S - 1 - e;
     const int opos = fwd ? hpos : hpos - T::dy(s) * G::HW - T::dx(s);
     bo[e] = 0.0;
-    if (b_old && Wt[s * G::NPW + opos] != 0.0) {
+    if (b_old && Wt[opos * G::S + s] != 0.0) {
       if constexpr (G::kStageB) {
-        bo[e] = Bo[(s * G::NO + opos) * D + c];
+        bo[e] = Bo[(opos * G::S + s) * D + c];
       } else {
         const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
         // kNc: b_old is read-only for this launch (multi-kernel path: the
@@ -343,7 +328,7 @@ __device__ __forceinline__ double tile_sb_element(const Grid<R>& g, const double
     const int npos = fwd ? hpos + T::dy(s) * G::HW + T::dx(s) : hpos - T::dy(s) * G::HW - T::dx(s);
     const int opos = fwd ? hpos : npos;  // owner = first endpoint i
     const int jpos = fwd ? npos : hpos;
-    const double w = Wt[s * G::NPW + opos];
+    const double w = Wt[opos * G::S + s];
     if (w == 0.0) continue;
     const double nw = -w;
     const double my = w * P[opos * D + c] + nw * P[jpos * D + c];
@@ -366,18 +351,18 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, S
   using T = GridTopo<R>;
   extern __shared__ double smem[];
   double* P = smem;                 // Y halo [NP][D]
-  double* Wt = P + G::NP * D;       // [S][NP]
-  double* Rq = Wt + G::S * G::NPW;   // rq interior [NV][D]
-  double* Bo = Rq + G::NV * D;      // b_old of owners [S][NO][D] (8-nbr only)
+  double* Wt = smem + G::kB_W;      // weights [NP][S]
+  double* Rq = smem + G::kB_Rq;     // rq interior [NV][D]
+  double* Bo = smem + G::kB_Bo;     // b_old of owners [NO][S][D] (8-nbr only)
   const int nt = num_tiles<R, D>(g);
   int bad = 0;
   for (int t = blockIdx.x; t < nt; t += gridDim.x) {
     const TileIdx ti = tile_of<R, D>(g, t);
     stage_rows<R, D, D>(g, ti, a.y, P, G::HH);
-    stage_planes<R, D, G::S, 1>(g, ti, g.wf, Wt, G::HH, G::NPW);
+    stage_rows<R, D, G::S>(g, ti, g.wf, Wt, G::HH);
     if (a.rhs) stage_interior<R, D, D>(g, ti, a.rq, Rq);
     if constexpr (G::kStageB) {
-      if (a.b_old) stage_planes<R, D, G::S, D>(g, ti, a.b_old, Bo, G::TH + R, G::NO);
+      if (a.b_old) stage_rows<R, D, G::S * D>(g, ti, a.b_old, Bo, G::TH + R);
     }
     cp_async_wait_all();
     __syncthreads();

@@ -204,6 +204,32 @@ def test_persistent_kernel_matches_multi_kernel_path(radius, d, kind):
     assert np.abs(st.split_b - full["split_b"]).max() <= 1e-9
 
 
+@pytest.mark.parametrize("h,w,radius,d", [(33, 70, 2, 8), (21, 64, 2, 4), (47, 38, 2, 2), (30, 71, 2, 4), (40, 66, 1, 4)])
+def test_tiled_persistent_tma_staging_bitwise(h, w, radius, d, monkeypatch):
+    """The tiled persistent kernel stages 5x5-grid tiles with TMA boxes (even
+    d and width) or cp.async (PFE_TMA=0, odd width, 8-neighbour grids):
+    staging must not change a single bit; ragged tiles at the right / bottom
+    edges are zero-filled by both."""
+    g = small_image(h, w, seed=h * w, radius=radius, sigma_xy=2.0 if radius == 2 else None)
+    prm = jacobi(d, soc=2, sb=5)
+    y0 = api.random_embedding(g.n, d, 2, g.degree)
+    out = {}
+    for flag in ("1", "0"):
+        if flag == "1":
+            monkeypatch.delenv("PFE_TMA", raising=False)  # default staging (TMA for 5x5 grids)
+        else:
+            monkeypatch.setenv("PFE_TMA", "0")
+        s = api.PfeSolver(g, prm, warn=False, persistent="tiled")
+        st = s.make_state(y0)
+        s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
+        assert s.report()["persistent_kind"] == 1
+        out[flag] = (st.y, st.split_b, st.split_s)
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+    exp = O.solve(g, prm, y0, mode=0)
+    assert rel_fro_signed(out["1"][0], exp) <= 1e-10
+
+
 @pytest.mark.parametrize("h,w,radius,d", [(1, 200, 1, 4), (300, 4, 1, 4), (5, 300, 2, 4), (17, 6, 2, 2),
                                             (150, 151, 1, 4), (3, 4, 1, 1)])
 def test_resident_kernel_region_shapes(h, w, radius, d):
