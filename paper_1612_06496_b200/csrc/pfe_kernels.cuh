@@ -245,14 +245,40 @@ __device__ __forceinline__ bool update_prologue(const PcgArgs& a, ColView<D>& cv
   return true;  // even with every column failed, write (inert) partials
 }
 
+// Vertex rows of a gather-bound kernel.  kContig (general graphs): each
+// block takes one contiguous range of (vertex, column group) items, so the
+// successive chunks a block (and its SM) processes are neighbours in the
+// locality storage order and share gathered rows in L1 (SpMV-type kernels).
+// Otherwise grid-stride order: the whole GPU sweeps one window of the
+// storage order, so an edge row read by both endpoints is still in L2 for
+// the second read (split-Bregman pass).
+template <int TPV, bool kContig = true, class Topo>
+__device__ __forceinline__ void row_range(const Topo& topo, long& e0, long& e1, long& step) {
+  const long first = static_cast<long>(topo.vbeg()) * TPV, total = static_cast<long>(topo.vend()) * TPV;
+  if constexpr (Topo::kGrid || !kContig) {
+    e0 = first + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    e1 = total;
+    step = static_cast<long>(gridDim.x) * blockDim.x;
+  } else {
+    const long cnt = total - first;
+    const long per = ((cnt + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x * blockDim.x;
+    e0 = first + static_cast<long>(blockIdx.x) * per + threadIdx.x;
+    e1 = first + static_cast<long>(blockIdx.x + 1) * per;
+    e1 = e1 < total ? e1 : total;
+    step = blockDim.x;
+  }
+}
+
 // ---------------------------------------------------------------- PCG init --
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock, 3) k_pcg_init(Topo topo, PcgArgs a) {
+__global__ void __launch_bounds__(kBlock, 2) k_pcg_init(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   double acc[3][V] = {};
   const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  long e0, e1, step;
+  row_range<TPV>(topo, e0, e1, step);
+  for (long e = e0; e < e1; e += step) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double ax[V] = {};
@@ -308,7 +334,9 @@ __global__ void __launch_bounds__(kBlock) k_pcg_pdir(Topo topo, PcgArgs a) {
   const double* pold = pcg_pold(a);
   const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  long e0, e1, step;
+  row_range<TPV>(topo, e0, e1, step);
+  for (long e = e0; e < e1; e += step) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     const Row<V> rv = ldg_row<V>(a.r + static_cast<long>(v) * D + c0);
@@ -323,7 +351,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_pdir(Topo topo, PcgArgs a) {
 
 // ------------------------------------------------------- PCG SpMV (+ p update)
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock, 3) k_pcg_spmv(Topo topo, PcgArgs a) {
+__global__ void __launch_bounds__(kBlock, 2) k_pcg_spmv(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   __shared__ ColView<D> cv;
   if (!spmv_prologue<D, kBlock>(a, cv)) return;
@@ -337,7 +365,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_pcg_spmv(Topo topo, PcgArgs a) {
   double acc[1][V] = {};
   const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  long e0, e1, step;
+  row_range<TPV>(topo, e0, e1, step);
+  for (long e = e0; e < e1; e += step) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double q[V] = {};
@@ -515,7 +545,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_sb_pass(Topo topo, SbArgs a) {
   const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   int bad = 0;
-  for (long e = static_cast<long>(topo.vbeg()) * TPV + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  long e0, e1, step;
+  row_range<TPV, false>(topo, e0, e1, step);
+  for (long e = e0; e < e1; e += step) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     const Row<V> yv = ldg_row<V>(a.y + static_cast<long>(v) * D + c0);
