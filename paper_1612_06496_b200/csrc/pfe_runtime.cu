@@ -18,6 +18,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <tuple>
@@ -96,6 +97,35 @@ void retain_pool_memory(int dev) {
   uint64_t keep = ~static_cast<uint64_t>(0);
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   done[dev] = true;
+}
+
+// Process-wide pool of pinned host control blocks: cudaMallocHost /
+// cudaFreeHost cost milliseconds each (cudaFreeHost synchronizes the
+// device), which showed up as ~7 ms per pfe_solve call on small graphs.
+struct PinnedCtlPool {
+  std::mutex mu;
+  std::vector<void*> free_list;
+  void* get(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!free_list.empty()) {
+        void* p = free_list.back();
+        free_list.pop_back();
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+  }
+  void put(void* p) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_list.push_back(p);
+  }
+};
+PinnedCtlPool& pinned_ctl_pool() {
+  static PinnedCtlPool* pool = new PinnedCtlPool();  // never destroyed: no CUDA calls at exit
+  return *pool;
 }
 
 struct DevPool {
@@ -295,7 +325,7 @@ struct pfe_solver {
     if (comm && g_comm_destroy) g_comm_destroy(comm);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_ctl) pinned_ctl_pool().put(h_ctl);
     if (aux) cudaStreamDestroy(aux);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -725,7 +755,8 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
   S->partials_c = S->mem.alloc<double>(static_cast<size_t>(S->sm) * 6 * pfe_dev::kMaxD);
   S->ctl = S->mem.alloc<Ctl>(1);
   CK(cudaMemsetAsync(S->ctl, 0, sizeof(Ctl), S->stream));
-  CK(cudaMallocHost(&S->h_ctl, sizeof(Ctl)));
+  S->h_ctl = static_cast<Ctl*>(pinned_ctl_pool().get(sizeof(Ctl)));
+  if (!S->h_ctl) throw Error(PFE_CUDA_ERROR, "cudaMallocHost failed for the control block");
   CK(cudaEventCreate(&S->ev0));
   CK(cudaEventCreate(&S->ev1));
   std::memset(S->h_ctl, 0, sizeof(Ctl));
