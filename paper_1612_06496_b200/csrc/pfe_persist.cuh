@@ -71,6 +71,8 @@ struct PersistArgs {
   // tiled persistent kernel: phases staging their tiles with TMA (bit 0
   // init, 1 SpMV, 2 split-Bregman pass, 3 b_old owner rows) or cp.async
   int tma;
+  // 8-neighbour grids (no TMA): halo rows staged as cp.async.bulk row copies
+  int bulk;
   TileMaps tm;
 };
 
@@ -122,15 +124,17 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
   // expected phase parity (identical in every thread)
   __shared__ alignas(8) uint64_t tbar[2];
   const bool tma_any = a.tma != 0;
+  const bool bulk_any = a.bulk != 0;
   uint32_t tph = 0;
-  if (tma_any && threadIdx.x == 0) {
+  if ((tma_any || bulk_any) && threadIdx.x == 0) {
     mbar_init(&tbar[0], 1);
     mbar_init(&tbar[1], 1);
     mbar_fence_init();
   }
   __syncthreads();
+  const bool bulk = a.bulk != 0;
   auto tile_wait = [&](bool tma, int buf, bool more) {
-    if (tma) {
+    if (tma || bulk) {
       mbar_wait(&tbar[buf], (tph >> buf) & 1u);
       tph ^= 1u << buf;
     }
@@ -176,6 +180,25 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
           }
           return;
         }
+        if (bulk) {
+          const Span sh = box_span(g, ti.x0 - R, ti.y0 - R, G::HW, G::HH, g.H);
+          const Span si = box_span(g, ti.x0, ti.y0, G::TW, G::TH, g.row_hi);
+          if (threadIdx.x < 32) {
+            if (threadIdx.x == 0) {
+              fence_proxy_async();
+              mbar_expect_tx(&tbar[buf], span_bytes<D>(sh) + span_bytes<G::S>(sh) + span_bytes<D>(si));
+            }
+            __syncwarp();
+            span_issue<D, G::HW>(g, sh, x0, P, &tbar[buf], threadIdx.x);
+            span_issue<G::S, G::HW>(g, sh, g.cf, Wt, &tbar[buf], threadIdx.x);
+            span_issue<D, G::TW>(g, si, rhs, Bv, &tbar[buf], threadIdx.x);
+          }
+          span_zero<D, G::HW, NT>(sh, P, G::HH);
+          span_zero<G::S, G::HW, NT>(sh, Wt, G::HH);
+          stage_interior<R, D, 1>(g, ti, g.diag, Dg);
+          stage_interior<R, D, 1>(g, ti, g.invd, Iv);
+          return;
+        }
         stage_rows<R, D, D>(g, ti, x0, P, G::HH);
         stage_rows<R, D, G::S>(g, ti, g.cf, Wt, G::HH);
         stage_interior<R, D, D>(g, ti, rhs, Bv);
@@ -207,6 +230,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
           acc[1][k] += rr * rr;
           acc[2][k] += rr * z;
         });
+        if (bulk) fence_proxy_async();  // zero-fill stores before later async writes
         __syncthreads();
         buf ^= 1;
       }
@@ -280,6 +304,27 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
             }
             return;
           }
+          if (bulk) {
+            const Span sh = box_span(g, ti.x0 - R, ti.y0 - R, G::HW, G::HH, g.H);
+            if (threadIdx.x < 32) {
+              if (threadIdx.x == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&tbar[buf], span_bytes<D>(sh) * (first ? 1u : 2u) + span_bytes<G::S>(sh));
+              }
+              __syncwarp();
+              span_issue<D, G::HW>(g, sh, pold, P, &tbar[buf], threadIdx.x);
+              if (!first) span_issue<D, G::HW>(g, sh, a.r, Rs, &tbar[buf], threadIdx.x);
+              span_issue<G::S, G::HW>(g, sh, g.cf, Wt, &tbar[buf], threadIdx.x);
+            }
+            span_zero<D, G::HW, NT>(sh, P, G::HH);
+            if (!first) {
+              span_zero<D, G::HW, NT>(sh, Rs, G::HH);
+              stage_rows<R, D, 1>(g, ti, g.invd, Iv, G::HH);
+            }
+            span_zero<G::S, G::HW, NT>(sh, Wt, G::HH);
+            stage_interior<R, D, 1>(g, ti, g.diag, Dg);
+            return;
+          }
           stage_rows<R, D, D>(g, ti, pold, P, G::HH);
           if (!first) {
             stage_rows<R, D, D>(g, ti, a.r, Rs, G::HH);
@@ -318,7 +363,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
           });
           // p' was formed in place (generic proxy); a later TMA copy into
           // this buffer (async proxy) must be ordered after those writes
-          if (tma) fence_proxy_async();
+          if (tma || bulk) fence_proxy_async();
           __syncthreads();
           buf ^= 1;
         }
@@ -503,6 +548,29 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
           }
           return;
         }
+        if (bulk) {
+          const Span sh = box_span(g, ti.x0 - R, ti.y0 - R, G::HW, G::HH, g.H);
+          const Span sb = box_span(g, ti.x0 - R, ti.y0 - R, G::HW, G::TH + R, g.H);
+          const Span si = box_span(g, ti.x0, ti.y0, G::TW, G::TH, g.row_hi);
+          const bool stage_b = G::kStageB && b_old;
+          if (threadIdx.x < 32) {
+            if (threadIdx.x == 0) {
+              fence_proxy_async();
+              mbar_expect_tx(&tbar[buf], span_bytes<D>(sh) + span_bytes<G::S>(sh) + (rhs_out ? span_bytes<D>(si) : 0u) +
+                                             (stage_b ? span_bytes<G::S * D>(sb) : 0u));
+            }
+            __syncwarp();
+            span_issue<D, G::HW>(g, sh, y, P, &tbar[buf], threadIdx.x);
+            span_issue<G::S, G::HW>(g, sh, g.wf, Wt, &tbar[buf], threadIdx.x);
+            if (rhs_out) span_issue<D, G::TW>(g, si, a.rq, Rq, &tbar[buf], threadIdx.x);
+            if constexpr (G::kStageB) {
+              if (stage_b) span_issue<G::S * D, G::HW>(g, sb, b_old, Bo, &tbar[buf], threadIdx.x);
+            }
+          }
+          span_zero<D, G::HW, NT>(sh, P, G::HH);
+          span_zero<G::S, G::HW, NT>(sh, Wt, G::HH);
+          return;
+        }
         stage_rows<R, D, D>(g, ti, y, P, G::HH);
         stage_rows<R, D, G::S>(g, ti, g.wf, Wt, G::HH);
         if (rhs_out) stage_interior<R, D, D>(g, ti, a.rq, Rq);
@@ -532,9 +600,10 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
         for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
           bad |= !isfinite(P[hpos * D + c]);
           const double acc = tile_sb_element<D, R, false>(g, P, Wt, Bo, b_old, b_new, s_out, a.gamma, hpos, c, v,
-                                                       ti.y0 + hpos / G::HW - R);
+                                                       ti.y0 + hpos / G::HW - R, ti.x0 + hpos % G::HW - R);
           if (rhs_out) rhs_out[v * D + c] = a.hl * acc + Rq[tv * D + c];
         });
+        if (bulk) fence_proxy_async();  // zero-fill stores before later async writes
         __syncthreads();
         if constexpr (kDB) buf ^= 1;
       }

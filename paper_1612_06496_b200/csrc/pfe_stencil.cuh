@@ -19,6 +19,7 @@
 #pragma once
 
 #include "pfe_kernels.cuh"
+#include "pfe_tma.cuh"
 
 namespace pfe_dev {
 
@@ -107,6 +108,64 @@ __device__ __forceinline__ void stage_rows(const Grid<R>& g, TileIdx ti, const d
     long u;
     const bool in = halo_in<R, D>(g, ti, pos, u);
     cp_async(dst + pos * W + k, in ? src + u * W + k : src, in, CH * 8);
+  }
+}
+
+// Bulk staging (cp.async.bulk): row hy of a tile box is one contiguous run
+// of a row-major [H][W][K] array, so it is one bulk copy of its in-image
+// part instead of (BW * K / 2) 16-byte cp.async with per-element address
+// arithmetic.  Lanes of warp 0 issue one row each, after lane 0 posted the
+// bytes (span_bytes) on the buffer's mbarrier.  Positions outside the image
+// are zero-filled with ordinary stores by span_zero (border tiles only).
+struct Span {
+  int r0, r1;  // box rows [r0, r1) inside the image
+  int c0, c1;  // box columns [c0, c1) inside the image
+  int ylo, xlo;
+};
+// Box of bw x nrows positions with top-left image position (xlo, ylo); rows
+// at or past ymax and columns past W are outside.
+template <int R>
+__device__ __forceinline__ Span box_span(const Grid<R>& g, int xlo, int ylo, int bw, int nrows, int ymax) {
+  Span sp;
+  sp.ylo = ylo;
+  sp.xlo = xlo;
+  sp.r0 = ylo < 0 ? -ylo : 0;
+  sp.r1 = ylo + nrows > ymax ? ymax - ylo : nrows;
+  sp.c0 = xlo < 0 ? -xlo : 0;
+  sp.c1 = xlo + bw > g.W ? g.W - xlo : bw;
+  if (sp.r1 < sp.r0) sp.r1 = sp.r0;
+  if (sp.c1 < sp.c0) sp.c1 = sp.c0;
+  return sp;
+}
+template <int K>
+__device__ __forceinline__ uint32_t span_bytes(const Span& sp) {
+  return static_cast<uint32_t>((sp.r1 - sp.r0) * (sp.c1 - sp.c0) * K * 8);
+}
+template <int K, int BW, int R>
+__device__ __forceinline__ void span_issue(const Grid<R>& g, const Span& sp, const double* __restrict__ src,
+                                           double* dst, uint64_t* bar, int lane) {
+  if constexpr (K % 2 != 0) {
+    return;  // odd widths never stage in bulk (the host requires even d)
+  } else {
+  if (sp.c1 <= sp.c0) return;
+  const uint32_t bytes = static_cast<uint32_t>((sp.c1 - sp.c0) * K * 8);
+  for (int hy = sp.r0 + lane; hy < sp.r1; hy += 32) {
+    const long u = static_cast<long>(sp.ylo + hy) * g.W + (sp.xlo + sp.c0);
+    bulk_copy(dst + (hy * BW + sp.c0) * K, src + u * K, bytes, bar);
+  }
+  }
+}
+template <int K, int BW, int NT>
+__device__ __forceinline__ void span_zero(const Span& sp, double* dst, int nrows) {
+  if constexpr (K % 2 != 0) return;
+  if (sp.r0 == 0 && sp.r1 == nrows && sp.c0 == 0 && sp.c1 == BW) return;
+  constexpr int PER = K / 2 > 0 ? K / 2 : 1;
+  const int total = nrows * BW * PER;
+  for (int c = threadIdx.x; c < total; c += NT) {
+    const int pos = c / PER, k = (c - pos * PER) * 2;
+    const int hy = pos / BW, hx = pos - hy * BW;
+    if (hy < sp.r0 || hy >= sp.r1 || hx < sp.c0 || hx >= sp.c1)
+      *reinterpret_cast<double2*>(dst + pos * K + k) = make_double2(0.0, 0.0);
   }
 }
 
@@ -297,7 +356,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
 template <int D, int R, bool kNc>
 __device__ __forceinline__ double tile_sb_element(const Grid<R>& g, const double* P, const double* Wt, const double* Bo,
                                                   const double* __restrict__ b_old, double* b_new, double* s_out,
-                                                  double gamma, int hpos, int c, long v, int vy) {
+                                                  double gamma, int hpos, int c, long v, int vy, int vx) {
   using G = TileGeo<R, D>;
   using T = GridTopo<R>;
   double bo[2 * G::S];
@@ -307,7 +366,13 @@ __device__ __forceinline__ double tile_sb_element(const Grid<R>& g, const double
     const int s = fwd ? e - G::S : G::S - 1 - e;
     const int opos = fwd ? hpos : hpos - T::dy(s) * G::HW - T::dx(s);
     bo[e] = 0.0;
-    if (b_old && Wt[opos * G::S + s] != 0.0) {
+    // staged: only present edges are read (the staged owner rows may be
+    // stale for absent ones); global: every edge whose owner lies inside the
+    // stored rows has a slot (absent edges hold zeros and are skipped
+    // below), so the load needs no shared-memory weight first
+    const bool valid = G::kStageB ? Wt[opos * G::S + s] != 0.0
+                                  : (fwd || (vy - T::dy(s) >= 0 && vx - T::dx(s) >= 0 && vx - T::dx(s) < g.W));
+    if (b_old && valid) {
       if constexpr (G::kStageB) {
         bo[e] = Bo[(opos * G::S + s) * D + c];
       } else {
@@ -369,7 +434,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, S
     for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
       bad |= !isfinite(P[hpos * D + c]);
       const double acc = tile_sb_element<D, R, true>(g, P, Wt, Bo, a.b_old, a.b_new, a.s_out, a.gamma, hpos, c, v,
-                                                          ti.y0 + hpos / G::HW - R);
+                                                          ti.y0 + hpos / G::HW - R, ti.x0 + hpos % G::HW - R);
       if (a.rhs) a.rhs[v * D + c] = a.hl * acc + Rq[tv * D + c];
     });
     __syncthreads();

@@ -81,4 +81,13 @@ __device__ __forceinline__ void tma_rows(double* dst, const CUtensorMap* m, int 
   }
 }
 
+// One contiguous global -> shared copy (16-byte aligned, size a multiple of
+// 16) completing on an mbarrier.
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 }  // namespace pfe_dev

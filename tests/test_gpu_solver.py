@@ -204,21 +204,24 @@ def test_persistent_kernel_matches_multi_kernel_path(radius, d, kind):
     assert np.abs(st.split_b - full["split_b"]).max() <= 1e-9
 
 
-@pytest.mark.parametrize("h,w,radius,d", [(33, 70, 2, 8), (21, 64, 2, 4), (47, 38, 2, 2), (30, 71, 2, 4), (40, 66, 1, 4)])
+@pytest.mark.parametrize("h,w,radius,d", [(33, 70, 2, 8), (21, 64, 2, 4), (47, 38, 2, 2), (30, 71, 2, 4), (40, 66, 1, 4),
+                                          (37, 70, 1, 8), (31, 65, 1, 2), (9, 40, 1, 4)])
 def test_tiled_persistent_tma_staging_bitwise(h, w, radius, d, monkeypatch):
     """The tiled persistent kernel stages 5x5-grid tiles with TMA boxes (even
-    d and width) or cp.async (PFE_TMA=0, odd width, 8-neighbour grids):
-    staging must not change a single bit; ragged tiles at the right / bottom
-    edges are zero-filled by both."""
+    d and width) and 8-neighbour tiles with cp.async.bulk row copies (even
+    d), else per-element cp.async (PFE_TMA=0 PFE_BULK=0): staging must not
+    change a single bit; ragged and border tiles are zero-filled by all."""
     g = small_image(h, w, seed=h * w, radius=radius, sigma_xy=2.0 if radius == 2 else None)
     prm = jacobi(d, soc=2, sb=5)
     y0 = api.random_embedding(g.n, d, 2, g.degree)
     out = {}
     for flag in ("1", "0"):
-        if flag == "1":
-            monkeypatch.delenv("PFE_TMA", raising=False)  # default staging (TMA for 5x5 grids)
-        else:
+        if flag == "1":  # TMA boxes (5x5 grids, default) / bulk row copies (8-neighbour, PFE_BULK=1)
+            monkeypatch.delenv("PFE_TMA", raising=False)
+            monkeypatch.setenv("PFE_BULK", "1")
+        else:  # per-element cp.async
             monkeypatch.setenv("PFE_TMA", "0")
+            monkeypatch.setenv("PFE_BULK", "0")
         s = api.PfeSolver(g, prm, warn=False, persistent="tiled")
         st = s.make_state(y0)
         s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
