@@ -247,6 +247,17 @@ int pfe_kmeans(int32_t n, int32_t d, const double* points, int32_t k, uint64_t s
 int pfe_kmeans_device(int32_t n, int32_t d, const double* points, int32_t k, uint64_t seed, int32_t max_iter,
                       int32_t device, int32_t* labels);
 
+/* GMM initial embedding on the GPU (gmm_fit +
+ * init_embedding, init.cpp:45-170): k-means (20 iterations, seed) for the
+ * starting means, <= 50 EM iterations of a diagonal GMM on the n x 3
+ * features (row-major RGB triples, as imgio.cpp produces them), then the
+ * responsibilities D-orthonormalised (Gram-Schmidt in <u, v> = u^T D v,
+ * noise fallback of init.cpp:160-168).  Replaces the host init path of
+ * main.cpp:109-110.  y_out: n x k column-major; means_out / vars_out
+ * (k x 3 row-major) and weights_out (k) may be null.  1 <= k <= 16. */
+int pfe_gmm_init_device(int32_t n, const double* features, int32_t k, uint64_t seed, const double* degree,
+                        int32_t device, double* y_out, double* means_out, double* vars_out, double* weights_out);
+
 /* k-NN graph builder for point sets (configs C1 / C5).  No reference
  * counterpart: the reference has no k-NN builder; this
  * is the harness definition of paper_1612_06496_b200/inputs.py knn_graph --

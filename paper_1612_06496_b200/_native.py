@@ -95,6 +95,7 @@ _SIGS = {
     "pfe_random_embedding": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _D, _D]),
     "pfe_kmeans": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_int32, C.c_uint64, C.c_int32, _I]),
     "pfe_kmeans_device": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_int32, C.c_uint64, C.c_int32, C.c_int32, _I]),
+    "pfe_gmm_init_device": (C.c_int, [C.c_int32, _D, C.c_int32, C.c_uint64, _D, C.c_int32, _D, _D, _D, _D]),
     "pfe_knn_graph": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_int32, C.c_int32, _I, _I, _D, _D,
                                 C.POINTER(C.c_int64), _D]),
 }

@@ -483,6 +483,26 @@ def kmeans(points, k: int, seed: int, max_iter: int = 100, device: Optional[int]
     return lab
 
 
+def gmm_init_embedding(features, k: int, seed: int, degree, device: int = 0, model: bool = False):
+    """GMM initial embedding on the GPU (init.cpp:45-170: gmm_fit + init_embedding;
+    pfe_gmm_init_device): k-means start, EM on the n x 3 features, then the
+    responsibilities D-orthonormalised.  Returns Y0 (n x k), and with
+    model=True also (means k x 3, variances k x 3, weights k)."""
+    f = np.ascontiguousarray(features, dtype=np.float64).reshape(-1, 3)
+    n = f.shape[0]
+    deg = np.ascontiguousarray(degree, dtype=np.float64)
+    if deg.shape != (n,):
+        raise ConfigError("gmm_init_embedding: degree must have one entry per point")
+    y = np.empty(n * int(k))
+    means, var, wts = np.empty(3 * int(k)), np.empty(3 * int(k)), np.empty(int(k))
+    _check(N.load().pfe_gmm_init_device(n, N.dptr(f), int(k), int(seed), N.dptr(deg), int(device), N.dptr(y),
+                                        N.dptr(means), N.dptr(var), N.dptr(wts)))
+    y0 = _from_colmajor(y, n, int(k))
+    if model:
+        return y0, means.reshape(-1, 3), var.reshape(-1, 3), wts
+    return y0
+
+
 def knn_graph_gpu(points, k: int, device: int = 0) -> "WeightedGraph":
     """Union-symmetrised k-NN heat-kernel graph built on the GPU (pfe_knn_graph);
     same definition as inputs.knn_graph (the host builder)."""

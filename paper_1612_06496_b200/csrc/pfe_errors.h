@@ -18,6 +18,8 @@ void d_orthonormalize(int n, int d, const double* a, const double* deg, double* 
 void kmeans(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
 void knn_search(int n, int dim, const double* pts, int k, double* d2, int32_t* idx);
 void kmeans_device(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
+void gmm_init_device(int n, const double* feat, int k, uint64_t seed, const double* degree, double* y_out,
+                     double* means_out, double* vars_out, double* weights_out);
 long knn_graph_from_lists(int n, int k, const double* d2, const int32_t* idx, int32_t* ei, int32_t* ej, double* w,
                           double* degree, double* sigma_out);
 

@@ -1840,6 +1840,14 @@ int pfe_kmeans_device(int32_t n, int32_t d, const double* points, int32_t k, uin
   });
 }
 
+int pfe_gmm_init_device(int32_t n, const double* features, int32_t k, uint64_t seed, const double* degree,
+                        int32_t device, double* y_out, double* means_out, double* vars_out, double* weights_out) {
+  return guarded([&] {
+    require_device(device);
+    pfe_host::gmm_init_device(n, features, k, seed, degree, y_out, means_out, vars_out, weights_out);
+  });
+}
+
 int pfe_knn_graph(int32_t n, int32_t dim, const double* points, int32_t k, int32_t device, int32_t* ei, int32_t* ej,
                   double* w, double* degree, int64_t* m_out, double* sigma_out) {
   return guarded([&] {
