@@ -34,9 +34,13 @@ extern "C" {
 #define PFE_CONFIG_ERROR 3
 #define PFE_CUDA_ERROR 4
 
-/* Preconditioner ids (pcg.hpp:13).  Ic0 runs the Jacobi path on the GPU and
- * reports jacobi_fallback = 1, exactly as the reference does when its IC(0)
- * factorization breaks down (pcg.cpp:22-28). */
+/* Preconditioner ids (pcg.hpp:13).  Ic0 (the reference default) on a
+ * single-GPU solver: the reference's IC(0) factor (sparse.cpp:124-203, host
+ * set-up) applied by level-scheduled device triangular solves, host-driven
+ * PCG loop on the general-graph kernels.  A factor that breaks down after
+ * every shift runs Jacobi and reports jacobi_fallback = 1, as the reference
+ * does (pcg.cpp:22-28); so do the row-band / vertex-range solvers and the
+ * one-shot pfe_pcg_solve_multi / pfe_split_bregman_standalone entry points. */
 #define PFE_PRECOND_IC0 0
 #define PFE_PRECOND_JACOBI 1
 #define PFE_PRECOND_NONE 2
@@ -116,7 +120,7 @@ typedef struct pfe_report {
 
 /* Per-kernel-class timing when pfe_exec.profile = 1. */
 #define PFE_KERNEL_CLASSES 8
-/* 0 pcg_init, 1 pcg_spmv, 2 pcg_update, 3 pcg_finalize, 4 sb_pass,
+/* 0 pcg_init, 1 pcg_spmv, 2 pcg_update (+ IC(0) triangular solves), 3 pcg_finalize, 4 sb_pass,
  * 5 rhs (quad / from state), 6 projection (tsqr + apply),
  * 7 persistent split-Bregman kernel */
 typedef struct pfe_kernel_times {

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace pfe_host {
 
@@ -18,6 +19,16 @@ void d_orthonormalize(int n, int d, const double* a, const double* deg, double* 
 void kmeans(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
 void knn_search(int n, int dim, const double* pts, int k, double* d2, int32_t* idx);
 void kmeans_device(int n, int d, const double* pts, int k, uint64_t seed, int max_iter, int32_t* labels);
+// IC(0) factor L (A ~ L L^T) of a natural-order CSR matrix, exactly as
+// incomplete_cholesky (sparse.cpp:124-203): lower triangle with a diagonal
+// shift, row-oriented sweep, shift retries.  false: breakdown persisted
+// (the reference then falls back to Jacobi, pcg.cpp:22-28).
+struct IcFactorHost {
+  std::vector<int> ptr, idx;  // rows of L, ascending columns, diagonal last
+  std::vector<double> val;
+  double shift = 0.0;
+};
+bool ic0_factor(int n, const int* ptr, const int* idx, const double* val, IcFactorHost& out);
 void gmm_init_device(int n, const double* feat, int k, uint64_t seed, const double* degree, double* y_out,
                      double* means_out, double* vars_out, double* weights_out);
 long knn_graph_from_lists(int n, int k, const double* d2, const int32_t* idx, int32_t* ei, int32_t* ej, double* w,

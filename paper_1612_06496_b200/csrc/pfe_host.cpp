@@ -179,4 +179,71 @@ void kmeans(int n_, int d_, const double* pts, int k_, uint64_t seed, int max_it
   }
 }
 
+// ------------------------------------------------------------ IC(0) ------
+// sparse.cpp:124-203.  The factor is set-up for the device triangular solves
+// (pfe_runtime.cu, k_ic_apply); the per-row arithmetic (sparse dot over the
+// columns below j, pivot sqrt, off-diagonal division) follows the reference
+// operation for operation, so the factor is the reference's bit for bit.
+namespace {
+bool ic0_sweep(IcFactorHost& l, int n) {
+  for (int i = 0; i < n; ++i) {
+    const int b = l.ptr[i], e = l.ptr[i + 1];
+    if (b == e || l.idx[e - 1] != i) return false;  // no diagonal
+    for (int k = b; k < e; ++k) {
+      const int j = l.idx[k];
+      double dot = 0.0;
+      int pi = b, pj = l.ptr[j];
+      const int ej = l.ptr[j + 1];
+      while (pi < k && pj < ej && l.idx[pj] < j) {
+        const int ci = l.idx[pi], cj = l.idx[pj];
+        if (ci == cj) {
+          dot += l.val[pi] * l.val[pj];
+          ++pi;
+          ++pj;
+        } else if (ci < cj) {
+          ++pi;
+        } else {
+          ++pj;
+        }
+      }
+      if (j == i) {
+        const double piv = l.val[k] - dot;
+        if (!(piv > 0.0)) return false;
+        l.val[k] = std::sqrt(piv);
+      } else {
+        l.val[k] = (l.val[k] - dot) / l.val[l.ptr[j + 1] - 1];
+      }
+    }
+  }
+  return true;
+}
+}  // namespace
+
+bool ic0_factor(int n, const int* ptr, const int* idx, const double* val, IcFactorHost& out) {
+  double dmax = 0.0;
+  for (int r = 0; r < n; ++r)
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k)
+      if (idx[k] == r) dmax = std::max(dmax, val[k]);
+  double shift = 0.0;
+  for (int attempt = 0; attempt <= 8; ++attempt) {
+    IcFactorHost l;
+    l.shift = shift;
+    l.ptr.assign(static_cast<size_t>(n) + 1, 0);
+    for (int r = 0; r < n; ++r) {
+      for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+        if (idx[k] > r) continue;
+        l.idx.push_back(idx[k]);
+        l.val.push_back(idx[k] == r ? val[k] + shift : val[k]);
+      }
+      l.ptr[r + 1] = static_cast<int>(l.val.size());
+    }
+    if (ic0_sweep(l, n)) {
+      out = std::move(l);
+      return true;
+    }
+    shift = shift == 0.0 ? 1e-3 * std::max(dmax, 1.0) : 2.0 * shift;
+  }
+  return false;
+}
+
 }  // namespace pfe_host

@@ -57,6 +57,9 @@ struct PcgArgs {
   // every band ([rank][pair], nb = ranks) instead of this grid's block partials.
   int rank_major;
   int skip_pdir;  // host side: pcg_spmv does not launch the CSR direction pass
+  // IC(0): z = M^-1 r of the latest update (the direction pass then forms
+  // p' = z + beta p, pcg.cpp:86-88); null: Jacobi z = D^-1 r on the fly
+  const double* zbuf;
   // Producer-side totals (single-domain solvers): the last block of each
   // producer reduces the block partials in a fixed order and writes the NQ*D
   // totals to tot_a (init / update) or tot_b (spmv); consumers then read
@@ -339,12 +342,18 @@ __global__ void __launch_bounds__(kBlock) k_pcg_pdir(Topo topo, PcgArgs a) {
   for (long e = e0; e < e1; e += step) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
-    const Row<V> rv = ldg_row<V>(a.r + static_cast<long>(v) * D + c0);
     const Row<V> po = ldg_row<V>(pold + static_cast<long>(v) * D + c0);
-    const double id = topo.inv_diag(v);
     Row<V> pu;
+    if (a.zbuf) {
+      const Row<V> zv = ldg_row<V>(a.zbuf + static_cast<long>(v) * D + c0);
 #pragma unroll
-    for (int k = 0; k < V; ++k) pu.a[k] = id * rv.a[k] + beta[k] * po.a[k];
+      for (int k = 0; k < V; ++k) pu.a[k] = zv.a[k] + beta[k] * po.a[k];
+    } else {
+      const Row<V> rv = ldg_row<V>(a.r + static_cast<long>(v) * D + c0);
+      const double id = topo.inv_diag(v);
+#pragma unroll
+      for (int k = 0; k < V; ++k) pu.a[k] = id * rv.a[k] + beta[k] * po.a[k];
+    }
     st_row<V>(pnew + static_cast<long>(v) * D + c0, pu);
   }
 }

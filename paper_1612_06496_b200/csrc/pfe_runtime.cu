@@ -22,6 +22,7 @@
 #include <numeric>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "pfe_b200.h"
@@ -239,6 +240,24 @@ struct GraphCache {
 // Set when NCCL is loaded (row-band solvers own a communicator).
 static void (*g_comm_destroy)(void*) = nullptr;
 
+// Device view of an IC(0) factor (see k_ic_apply).
+struct IcDev {
+  const int* pos;    // natural row -> storage position
+  const int* fptr;   // rows of L (natural), ascending columns, diagonal last
+  const int* fcol;   // storage position of the column
+  const double* fval;
+  const int* frows;  // natural rows by forward level
+  const int* flev;   // [nlf + 1]
+  int nlf;
+  const int* bptr;   // columns of L below the diagonal, descending row
+  const int* bcol;   // storage position of that row
+  const double* bval;
+  const double* bdg;  // L_jj (natural j)
+  const int* brows;
+  const int* blev;
+  int nlb;
+};
+
 struct pfe_solver {
   int device = 0;
   cudaStream_t stream = nullptr, aux = nullptr;
@@ -314,6 +333,11 @@ struct pfe_solver {
   long inner_launched = 0;  // host mirror of ctl->inner_count
   const LaunchTable* tab = nullptr;
   bool jacobi_fallback = false;
+  // IC(0) preconditioner (PFE_PRECOND_IC0 on single-GPU solvers): device
+  // factor + level schedules, and the z buffer of the PCG loop
+  bool ic = false;
+  IcDev icd{};
+  double* zbuf = nullptr;
   double setup_s = 0.0;
   int pred_iters = 1;
   Prof prof;
@@ -403,6 +427,77 @@ __global__ void k_grid_coef(long cnt, const double* __restrict__ wf, double hl, 
     const double w = wf[i];
     cf[i] = w != 0.0 ? -((hl * w) * w) : 0.0;
   }
+}
+
+// --------------------------------------------------- IC(0) preconditioner --
+// z = (L L^T)^-1 r with the reference's triangular solves (sparse.cpp:205-238),
+// level-scheduled: rows of one level are independent.  One block per
+// embedding column walks the levels with a block barrier in between (the
+// column's whole dependency chain stays inside one SM).  Forward: row i in
+// ascending column order, acc -= L_ik z_k, z_i = acc / L_ii.  Backward (the
+// reference scatters column i of L^T after dividing): z_j = (z_j - sum over
+// rows i > j in DESCENDING i of L_ij z_i) / L_jj -- the same subtractions in
+// the same order, gathered.
+
+template <int D>
+__global__ void __launch_bounds__(1024) k_ic_apply(IcDev ic, const double* __restrict__ r, double* z) {
+  const int c = blockIdx.x;
+  for (int l = 0; l < ic.nlf; ++l) {
+    for (int t = ic.flev[l] + threadIdx.x; t < ic.flev[l + 1]; t += blockDim.x) {
+      const int i = ic.frows[t];
+      const long pi = ic.pos[i];
+      double acc = r[pi * D + c];
+      const int b = ic.fptr[i], e = ic.fptr[i + 1] - 1;
+      for (int k = b; k < e; ++k) acc -= ic.fval[k] * z[static_cast<long>(ic.fcol[k]) * D + c];
+      z[pi * D + c] = acc / ic.fval[e];
+    }
+    __syncthreads();
+  }
+  for (int l = 0; l < ic.nlb; ++l) {
+    for (int t = ic.blev[l] + threadIdx.x; t < ic.blev[l + 1]; t += blockDim.x) {
+      const int j = ic.brows[t];
+      const long pj = ic.pos[j];
+      double acc = z[pj * D + c];
+      for (int k = ic.bptr[j]; k < ic.bptr[j + 1]; ++k) acc -= ic.bval[k] * z[static_cast<long>(ic.bcol[k]) * D + c];
+      z[pj * D + c] = acc / ic.bdg[j];
+    }
+    __syncthreads();
+  }
+}
+
+// tot[slot * D + j] = sum_v r_vj z_vj (pcg.cpp:66 / 85 with z = M^-1 r):
+// deterministic block partials, reduced by the last block.
+template <int D>
+__global__ void __launch_bounds__(256) k_ic_dot(int n, const double* __restrict__ r, const double* __restrict__ z,
+                                                double* part, pfe_dev::Ctl* ctl, double* tot) {
+  double acc[1][D] = {};
+  for (long v = blockIdx.x * 256L + threadIdx.x; v < n; v += static_cast<long>(gridDim.x) * 256) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[0][c] += r[v * D + c] * z[v * D + c];
+  }
+  pfe_dev::block_reduce_store<1, D, D, 256>(acc, part);
+  __shared__ double out[1][D];
+  if (pfe_dev::grid_reduce_last<1, D, 256>(part, ctl, out) && threadIdx.x < D) tot[threadIdx.x] = out[0][threadIdx.x];
+}
+
+template <int D>
+void ic_apply_d(const IcDev& ic, const double* r, double* z, cudaStream_t s) {
+  k_ic_apply<D><<<D, 1024, 0, s>>>(ic, r, z);
+}
+template <int D>
+void ic_dot_d(int n, const double* r, const double* z, double* part, pfe_dev::Ctl* ctl, double* tot, int grid,
+              cudaStream_t s) {
+  k_ic_dot<D><<<grid, 256, 0, s>>>(n, r, z, part, ctl, tot);
+}
+template <int... Ds>
+void ic_apply_dispatch(int d, std::integer_sequence<int, Ds...>, const IcDev& ic, const double* r, double* z,
+                       cudaStream_t s) {
+  ((d == Ds + 1 ? ic_apply_d<Ds + 1>(ic, r, z, s) : void()), ...);
+}
+template <int... Ds>
+void ic_dot_dispatch(int d, std::integer_sequence<int, Ds...>, int n, const double* r, const double* z, double* part,
+                     pfe_dev::Ctl* ctl, double* tot, int grid, cudaStream_t s) {
+  ((d == Ds + 1 ? ic_dot_d<Ds + 1>(n, r, z, part, ctl, tot, grid, s) : void()), ...);
 }
 
 struct HostGraph {
@@ -525,6 +620,79 @@ double* grid_coef(pfe_solver* S, const double* dwf, long cnt, double hl, cudaStr
   if (cnt > 0) k_grid_coef<<<std::max(1, grid), 256, 0, st>>>(cnt, dwf, hl, dcf);
   CK(cudaGetLastError());
   return dcf;
+}
+
+// IC(0) factor of A in the reference's (natural) row order, its level
+// schedules and device copy (columns as storage positions).  A factor that
+// breaks down after every shift falls back to Jacobi like the reference.
+void build_ic(pfe_solver* S, int n, const std::vector<int>& aptr, const std::vector<int>& acol,
+              const std::vector<double>& aval, const std::vector<int>& perm) {
+  pfe_host::IcFactorHost f;
+  if (!pfe_host::ic0_factor(n, aptr.data(), acol.data(), aval.data(), f)) {
+    S->ic = false;
+    S->jacobi_fallback = true;
+    return;
+  }
+  auto by_level = [n](const std::vector<int>& lev, int nl, std::vector<int>& rows, std::vector<int>& off) {
+    off.assign(static_cast<size_t>(nl) + 1, 0);
+    for (int i = 0; i < n; ++i) ++off[lev[i] + 1];
+    for (int l = 0; l < nl; ++l) off[l + 1] += off[l];
+    rows.assign(static_cast<size_t>(n), 0);
+    std::vector<int> fill(off.begin(), off.end() - 1);
+    for (int i = 0; i < n; ++i) rows[fill[lev[i]]++] = i;
+  };
+  // forward levels: 1 + the deepest column a row reads
+  std::vector<int> lev(static_cast<size_t>(n), 0);
+  int nlf = 0;
+  for (int i = 0; i < n; ++i) {
+    int l = 0;
+    for (int k = f.ptr[i]; k < f.ptr[i + 1] - 1; ++k) l = std::max(l, lev[f.idx[k]] + 1);
+    lev[i] = l;
+    nlf = std::max(nlf, l + 1);
+  }
+  std::vector<int> frows, flev;
+  by_level(lev, nlf, frows, flev);
+  std::vector<int> fcol(f.idx.size());
+  for (size_t k = 0; k < f.idx.size(); ++k) fcol[k] = perm[f.idx[k]];
+  // backward: below-diagonal entries of column j, rows descending
+  std::vector<int> bptr(static_cast<size_t>(n) + 1, 0);
+  for (int i = 0; i < n; ++i)
+    for (int k = f.ptr[i]; k < f.ptr[i + 1] - 1; ++k) ++bptr[f.idx[k] + 1];
+  for (int j = 0; j < n; ++j) bptr[j + 1] += bptr[j];
+  std::vector<int> bcol(static_cast<size_t>(bptr[n])), bfill(bptr.begin(), bptr.end() - 1);
+  std::vector<double> bval(static_cast<size_t>(bptr[n])), bdg(static_cast<size_t>(n));
+  std::vector<int> blv(static_cast<size_t>(n), 0);
+  int nlb = 0;
+  for (int i = n - 1; i >= 0; --i) {
+    nlb = std::max(nlb, blv[i] + 1);
+    for (int k = f.ptr[i]; k < f.ptr[i + 1] - 1; ++k) {
+      const int j = f.idx[k];
+      bcol[bfill[j]] = perm[i];
+      bval[bfill[j]++] = f.val[k];
+      blv[j] = std::max(blv[j], blv[i] + 1);
+    }
+  }
+  for (int j = 0; j < n; ++j) bdg[j] = f.val[f.ptr[j + 1] - 1];
+  std::vector<int> brows, blev;
+  by_level(blv, nlb, brows, blev);
+  cudaStream_t st = S->stream;
+  IcDev& d = S->icd;
+  d.pos = S->mem.upload(perm, st);
+  d.fptr = S->mem.upload(f.ptr, st);
+  d.fcol = S->mem.upload(fcol, st);
+  d.fval = S->mem.upload(f.val, st);
+  d.frows = S->mem.upload(frows, st);
+  d.flev = S->mem.upload(flev, st);
+  d.nlf = nlf;
+  d.bptr = S->mem.upload(bptr, st);
+  d.bcol = S->mem.upload(bcol, st);
+  d.bval = S->mem.upload(bval, st);
+  d.bdg = S->mem.upload(bdg, st);
+  d.brows = S->mem.upload(brows, st);
+  d.blev = S->mem.upload(blev, st);
+  d.nlb = nlb;
+  S->zbuf = S->mem.alloc<double>(static_cast<size_t>(n) * S->d);
+  CK(cudaStreamSynchronize(st));  // host vectors die here
 }
 
 void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad) {
@@ -687,6 +855,36 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     }
     aptr[x + 1] = static_cast<int>(acol.size());
   }
+  if (S->ic) {
+    // A in the reference's row order (the IC(0) factor depends on it)
+    std::vector<int> nptr(static_cast<size_t>(n) + 1, 0), ncol;
+    std::vector<double> nval;
+    ncol.reserve(acol.size());
+    nval.reserve(aval.size());
+    for (int v = 0; v < n; ++v) {
+      row.clear();
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k) row.emplace_back(inbr[k], -((hl * iw[k]) * iw[k]));
+      row.emplace_back(v, diag[v]);
+      std::stable_sort(row.begin(), row.end(),
+                       [](const std::pair<int, double>& a, const std::pair<int, double>& b) { return a.first < b.first; });
+      for (size_t t = 0; t < row.size();) {
+        const int col = row[t].first;
+        double s = 0.0;
+        if (col == v) {
+          s = row[t].second;
+          ++t;
+        } else {
+          for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
+        }
+        if (s != 0.0) {
+          ncol.push_back(col);
+          nval.push_back(s);
+        }
+      }
+      nptr[v + 1] = static_cast<int>(ncol.size());
+    }
+    build_ic(S, n, nptr, ncol, nval, perm);
+  }
   // edge storage follows the vertex storage order: the edges a vertex owns
   // (it is their first endpoint) are consecutive rows of the edge arrays
   std::vector<int> epos(static_cast<size_t>(m));
@@ -789,11 +987,19 @@ pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exe
   if (g->m > 0x3fffffffL) config_error("graph too large for 32-bit edge indices");
   auto S = std::make_unique<pfe_solver>();
   S->prm = *p;
-  S->jacobi_fallback = p->preconditioner == PFE_PRECOND_IC0;
+  // IC(0) (the reference default): general-graph kernels, host-driven PCG
+  // loop with the device triangular solves after init and every update
+  S->ic = p->preconditioner == PFE_PRECOND_IC0;
+  S->jacobi_fallback = false;
   init_common(S.get(), x, p->dim);
+  if (S->ic) {
+    S->use_graphs = false;
+    S->persistent = false;
+    S->resident = false;
+  }
   S->n = g->n;
   S->m = g->m;
-  build_topology(S.get(), hg, g->grid_h, g->grid_w, g->grid_radius);
+  build_topology(S.get(), hg, S->ic ? 0 : g->grid_h, S->ic ? 0 : g->grid_w, S->ic ? 0 : g->grid_radius);
   upload_degree(S.get(), g->degree);
   S->qr_blocks = qr_blocks_for(S.get(), g->n);
   S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * S->d * S->d);
@@ -930,7 +1136,8 @@ PcgArgs pcg_args(pfe_state* st, const double* rhs) {
   // has no serial tail.
   a.tot_a = S->totals;
   a.tot_b = S->totals + 3 * pfe_dev::kMaxD;
-  a.totals = S->topo.kind == pfe_host::kTopoCsr && static_cast<long>(S->n) * S->d >= (1L << 22);
+  a.totals = S->ic || (S->topo.kind == pfe_host::kTopoCsr && static_cast<long>(S->n) * S->d >= (1L << 22));
+  a.zbuf = S->ic ? S->zbuf : nullptr;
   if (a.totals) {
     a.rd_a = a.tot_a;
     a.rd_b = a.tot_b;
@@ -967,18 +1174,33 @@ void pcg_solve_host(pfe_state* st, const double* rhs) {
     S->tab->pcg_spmv(S->topo, a, L);
     S->prof.end(S->stream);
   };
+  // IC(0): z = M^-1 r by the device triangular solves, and the r.z total
+  // the consumers read (slot 2 after init, slot 1 after an update) replaced
+  // by the preconditioned one (pcg.cpp:63-66, 85-88)
+  using DSeq = std::make_integer_sequence<int, pfe_dev::kMaxD>;
+  auto ic_z = [&](double* z, int slot) {
+    if (!S->ic) return;
+    S->prof.begin(2, S->stream);  // timed with the update class
+    ic_apply_dispatch(S->d, DSeq{}, S->icd, a.r, z, S->stream);
+    const int grid = std::min(S->max_grid, std::max(1, (S->n + 255) / 256));
+    ic_dot_dispatch(S->d, DSeq{}, S->n, a.r, z, S->partials, S->ctl, a.tot_a + slot * S->d, grid, S->stream);
+    CK(cudaGetLastError());
+    S->prof.end(S->stream);
+  };
   auto update = [&](int k) {
     a.phase = pfe_dev::pcg_phase(k);
     S->prof.begin(2, S->stream);
     S->tab->pcg_update(S->topo, a, L);
     S->prof.end(S->stream);
+    ic_z(S->zbuf, 1);
   };
   S->prof.begin(0, S->stream);
   S->tab->pcg_init(S->topo, a, L);
   S->prof.end(S->stream);
+  ic_z(a.pbuf[0], 2);  // p = z for the first iteration
   int k = 1;
   spmv(1);
-  for (int burst = std::max(1, S->pred_iters);; burst = 1) {
+  for (int burst = S->ic ? 1 : std::max(1, S->pred_iters);; burst = 1) {
     for (int b = 1; b < burst && k <= maxit; ++b) {
       update(k);
       spmv(++k);
