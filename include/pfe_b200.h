@@ -40,7 +40,8 @@ extern "C" {
  * PCG loop on the general-graph kernels.  A factor that breaks down after
  * every shift runs Jacobi and reports jacobi_fallback = 1, as the reference
  * does (pcg.cpp:22-28); so do the row-band / vertex-range solvers and the
- * one-shot pfe_pcg_solve_multi / pfe_split_bregman_standalone entry points. */
+ * one-shot pfe_split_bregman_standalone entry point.  pfe_pcg_solve_multi
+ * (PcgOperator::solve_multi) factors the given matrix the same way. */
 #define PFE_PRECOND_IC0 0
 #define PFE_PRECOND_JACOBI 1
 #define PFE_PRECOND_NONE 2

@@ -1873,6 +1873,12 @@ int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_id
     S->topo.kind = pfe_host::kTopoCsr;
     S->topo.csr = c;
     S->edge_rows = 0;
+    if (preconditioner == PFE_PRECOND_IC0) {  // PcgOperator ctor, pcg.cpp:22-28
+      S->ic = true;
+      std::vector<int> ident(static_cast<size_t>(n));
+      std::iota(ident.begin(), ident.end(), 0);
+      build_ic(S.get(), n, aptr, acol, aval, ident);  // breakdown: Jacobi + jacobi_fallback
+    }
     std::unique_ptr<pfe_state> st(create_state(S.get(), x0));
     upload_rows(S.get(), b, n, d, st->r, st->q);
     S->ensure_log(1);
@@ -1886,7 +1892,7 @@ int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_id
       if (iterations) iterations[j] = col.iters;
       if (converged) converged[j] = ok ? 1 : 0;
       if (residual) residual[j] = col.rel;
-      if (jacobi_fallback) jacobi_fallback[j] = preconditioner == PFE_PRECOND_IC0 ? 1 : 0;
+      if (jacobi_fallback) jacobi_fallback[j] = S->jacobi_fallback ? 1 : 0;
     }
   });
 }

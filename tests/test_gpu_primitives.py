@@ -62,7 +62,7 @@ def test_projection_idempotent_scale_and_rank():
         api.project_orthogonal(np.ones((2, 3)))
 
 
-@pytest.mark.parametrize("prec", [api.Preconditioner.Jacobi, api.Preconditioner.NONE])
+@pytest.mark.parametrize("prec", [api.Preconditioner.Jacobi, api.Preconditioner.NONE, api.Preconditioner.Ic0])
 def test_pcg_solve_multi_matches_oracle_per_column(prec):
     """Equal per-column iteration counts and x to 1e-12."""
     rng = np.random.Generator(np.random.PCG64(23))
@@ -76,6 +76,7 @@ def test_pcg_solve_multi_matches_oracle_per_column(prec):
         xo, its, conv, res = O.pcg_solve_multi(a, b, x0, 1e-10, 500, int(prec))
         assert [r.iterations for r in reps] == list(its)
         assert all(r.converged for r in reps)
+        assert not any(r.jacobi_fallback for r in reps)
         assert np.abs(x - xo).max() <= 1e-12 * max(1.0, np.abs(xo).max())
 
 
