@@ -39,9 +39,9 @@ extern "C" {
  * set-up) applied by level-scheduled device triangular solves, host-driven
  * PCG loop on the general-graph kernels.  A factor that breaks down after
  * every shift runs Jacobi and reports jacobi_fallback = 1, as the reference
- * does (pcg.cpp:22-28); so do the row-band / vertex-range solvers and the
- * one-shot pfe_split_bregman_standalone entry point.  pfe_pcg_solve_multi
- * (PcgOperator::solve_multi) factors the given matrix the same way. */
+ * does (pcg.cpp:22-28); so do the row-band / vertex-range solvers.
+ * pfe_split_bregman_standalone and pfe_pcg_solve_multi
+ * (PcgOperator::solve_multi) factor their matrix the same way. */
 #define PFE_PRECOND_IC0 0
 #define PFE_PRECOND_JACOBI 1
 #define PFE_PRECOND_NONE 2

@@ -1817,12 +1817,18 @@ int pfe_split_bregman_standalone(const pfe_graph* g, const double* p, const doub
     auto S = std::make_unique<pfe_solver>();
     S->prm = local;
     S->warn = false;  // the standalone entry point does not warn (solver.cpp:161-180)
-    S->jacobi_fallback = local.preconditioner == PFE_PRECOND_IC0;
+    S->ic = local.preconditioner == PFE_PRECOND_IC0;  // solver.cpp:150-151 builds a PcgOperator
+    S->jacobi_fallback = false;
     init_common(S.get(), x, d);
     S->warn = false;
+    if (S->ic) {
+      S->use_graphs = false;
+      S->persistent = false;
+      S->resident = false;
+    }
     S->n = g->n;
     S->m = g->m;
-    build_topology(S.get(), hg, g->grid_h, g->grid_w, g->grid_radius);
+    build_topology(S.get(), hg, S->ic ? 0 : g->grid_h, S->ic ? 0 : g->grid_w, S->ic ? 0 : g->grid_radius);
     upload_degree(S.get(), g->degree);
     S->qr_blocks = 1;
     S->rbuf = S->mem.alloc<double>(static_cast<size_t>(d) * d);

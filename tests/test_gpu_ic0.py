@@ -84,3 +84,20 @@ def test_recorded_reference_run_on_gpu():
     seg = api.kmeans(y, 4, 0)
     truth = np.array([(r >= size // 2) * 2 + (c >= size // 2) for r in range(size) for c in range(size)], np.int32)
     assert O.covering(seg, truth) == pytest.approx(1.0, abs=5e-7)
+
+
+def test_ic0_standalone_split_bregman_matches_oracle():
+    """The free split_bregman (solver.cpp:138-182) builds its own PcgOperator
+    with the caller's config: IC(0) there too."""
+    rng = np.random.Generator(np.random.PCG64(12))
+    g = random_graph(50, 120, rng)
+    p, b = rng.uniform(-1, 1, (50, 3)), rng.uniform(-1, 1, (50, 3))
+    y_init = rng.uniform(-1, 1, (50, 3))
+    prm = ic0(3, lam=5.0, tol=1e-10, maxit=500)
+    traj = []
+    got = api.split_bregman(g, g.degree, p, b, prm, y_init, 6, on_iterate=lambda it, y: traj.append(y))
+    exp, exp_traj = O.split_bregman(g, g.degree, p, b, prm, y_init, 6, want_traj=True)
+    assert len(traj) == len(exp_traj) == 6
+    for a, c in zip(traj, exp_traj):
+        assert np.abs(a - c).max() <= 1e-10
+    assert np.abs(got - exp).max() <= 1e-10
