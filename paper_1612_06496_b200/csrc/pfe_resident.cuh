@@ -38,34 +38,10 @@ struct ResGeo {
   static constexpr int kMaxBlocks = 256;  // reduce_partials_warp limit
   static constexpr int S = GridTopo<R>::S;
   static constexpr int U = D;                     // units (pixel, column) per pixel
-  static constexpr int kPerPos = 3 * D + S + 2;  // shared doubles per ring/interior position
+  static constexpr int kPerPos = 3 * D + 2 * S + 2;  // shared doubles per ring/interior position
   static constexpr bool kFix = (32 % D == 0);
   static constexpr int V = kFix ? 1 : D;
 };
-
-// (A p)_v, column c, in the order of tile_apply_A (sparse.cpp:77-83), with a
-// runtime pitch.
-template <int D, int R>
-__device__ __forceinline__ double res_apply_A(double hl, const double* P, const double* Wt, int np, int hw, int hp,
-                                              int c, double diag_v) {
-  using T = GridTopo<R>;
-  constexpr int S = T::S;
-  double q = 0.0;
-#pragma unroll
-  for (int s = S - 1; s >= 0; --s) {
-    const int npos = hp - T::dy(s) * hw - T::dx(s);
-    const double w = Wt[s * np + npos];
-    if (w != 0.0) q += -((hl * w) * w) * P[npos * D + c];
-  }
-  q += diag_v * P[hp * D + c];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int npos = hp + T::dy(s) * hw + T::dx(s);
-    const double w = Wt[s * np + hp];
-    if (w != 0.0) q += -((hl * w) * w) * P[npos * D + c];
-  }
-  return q;
-}
 
 // Fixed-order reduction of nb <= 256 pair-major block partials into out[NQ][D]
 // (identical in every block): warp w sums pairs w, w + NT/32, ...; lane l
@@ -134,6 +110,7 @@ __global__ void __launch_bounds__(768, 1) k_sb_resident(PersistArgs<R> a) {
   double* Wt = A3 + NP * D;
   double* Iv = Wt + S * NP;
   double* Dg = Iv + NP;
+  double* Ct = Dg + NP;  // [S][NP] off-diagonal entries of A (Grid::cf), +0.0 = absent edge
 
   // this thread's interior elements e_k = tid + k NT, k < nk: smem position
   // hpk[k], column col(k), vertex vert(k); bit k of bnd: on the region boundary
@@ -176,18 +153,18 @@ __global__ void __launch_bounds__(768, 1) k_sb_resident(PersistArgs<R> a) {
       for (int j = 0; j < S; ++j) {  // backward slots S-1 .. 0
         const int s = S - 1 - j;
         const int pn = hp - T::dy(s) * HW - T::dx(s);
-        const double w = Wt[s * NP + pn];
-        nz[j] = w != 0.0;
-        t[j] = -((g.hl * w) * w) * Pc[pn * D];
+        const double cw = Ct[s * NP + pn];  // -((hl w) w); present edges have the sign bit set
+        nz[j] = __double_as_longlong(cw) < 0;
+        t[j] = cw * Pc[pn * D];
       }
       nz[S] = true;
       t[S] = Dg[hp] * Pc[hp * D];
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int pn = hp + T::dy(s) * HW + T::dx(s);
-        const double w = Wt[s * NP + hp];
-        nz[S + 1 + s] = w != 0.0;
-        t[S + 1 + s] = -((g.hl * w) * w) * Pc[pn * D];
+        const double cw = Ct[s * NP + hp];
+        nz[S + 1 + s] = __double_as_longlong(cw) < 0;
+        t[S + 1 + s] = cw * Pc[pn * D];
       }
       double acc = 0.0;
 #pragma unroll
@@ -258,7 +235,10 @@ __global__ void __launch_bounds__(768, 1) k_sb_resident(PersistArgs<R> a) {
       const long u = static_cast<long>(yy) * g.W + xx;
       const int hp = (ly + R) * HW + lx + R;
 #pragma unroll
-      for (int s = 0; s < S; ++s) Wt[s * NP + hp] = __ldg(g.wf + u * S + s);
+      for (int s = 0; s < S; ++s) {
+        Wt[s * NP + hp] = __ldg(g.wf + u * S + s);
+        Ct[s * NP + hp] = __ldg(g.cf + u * S + s);
+      }
       Iv[hp] = __ldg(g.invd + u);
       Dg[hp] = __ldg(g.diag + u);
 #pragma unroll
