@@ -241,21 +241,21 @@ struct GraphCache {
 static void (*g_comm_destroy)(void*) = nullptr;
 
 // Device view of an IC(0) factor (see k_ic_apply).
+struct IcSweep {
+  // rows of one triangular sweep in level order: slot t solves storage row
+  // spos[t] with sdg[t] and the slen[t] entries ecol/eval[sbeg[t] ...] in
+  // the reference's subtraction order; slots of level l: [lev[l], lev[l+1])
+  const int* spos;
+  const int* sbeg;
+  const int* slen;
+  const double* sdg;
+  const int* ecol;  // storage position of the operand row
+  const double* eval;
+  const int* lev;
+  int nl;
+};
 struct IcDev {
-  const int* pos;    // natural row -> storage position
-  const int* fptr;   // rows of L (natural), ascending columns, diagonal last
-  const int* fcol;   // storage position of the column
-  const double* fval;
-  const int* frows;  // natural rows by forward level
-  const int* flev;   // [nlf + 1]
-  int nlf;
-  const int* bptr;   // columns of L below the diagonal, descending row
-  const int* bcol;   // storage position of that row
-  const double* bval;
-  const double* bdg;  // L_jj (natural j)
-  const int* brows;
-  const int* blev;
-  int nlb;
+  IcSweep fwd, bwd;
 };
 
 struct pfe_solver {
@@ -439,30 +439,68 @@ __global__ void k_grid_coef(long cnt, const double* __restrict__ wf, double hl, 
 // rows i > j in DESCENDING i of L_ij z_i) / L_jj -- the same subtractions in
 // the same order, gathered.
 
+// One sweep.  Everything a slot needs that does not depend on z (its row,
+// length, diagonal and up to kIcPre entries) is loaded for the next level
+// while the current one computes, so a level costs one barrier plus the z
+// gathers of its rows (L1: the same block wrote them).
+constexpr int kIcPre = 8;
 template <int D>
-__global__ void __launch_bounds__(1024) k_ic_apply(IcDev ic, const double* __restrict__ r, double* z) {
+__device__ __forceinline__ void ic_sweep(const IcSweep& sw, const double* src, double* z, int c) {
+  struct Pre {
+    int pos, beg, len;
+    double dg;
+    int col[kIcPre];
+    double val[kIcPre];
+  };
+  auto fetch = [&](int t, Pre& p) {
+    p.pos = -1;
+    if (t < 0) return;
+    p.pos = sw.spos[t];
+    p.beg = sw.sbeg[t];
+    p.len = sw.slen[t];
+    p.dg = sw.sdg[t];
+#pragma unroll
+    for (int e = 0; e < kIcPre; ++e)
+      if (e < p.len) {
+        p.col[e] = sw.ecol[p.beg + e];
+        p.val[e] = sw.eval[p.beg + e];
+      }
+  };
+  auto solve = [&](const Pre& p) {
+    double acc = src[static_cast<long>(p.pos) * D + c];
+#pragma unroll
+    for (int e = 0; e < kIcPre; ++e)
+      if (e < p.len) acc -= p.val[e] * z[static_cast<long>(p.col[e]) * D + c];
+    for (int e = kIcPre; e < p.len; ++e)
+      acc -= sw.eval[p.beg + e] * z[static_cast<long>(sw.ecol[p.beg + e]) * D + c];
+    z[static_cast<long>(p.pos) * D + c] = acc / p.dg;
+  };
+  Pre cur, nxt;
+  fetch(sw.nl > 0 && threadIdx.x < sw.lev[1] - sw.lev[0] ? sw.lev[0] + static_cast<int>(threadIdx.x) : -1, cur);
+  for (int l = 0; l < sw.nl; ++l) {
+    const int b = sw.lev[l], e = sw.lev[l + 1];
+    if (l + 1 < sw.nl) {
+      const int t = sw.lev[l + 1] + static_cast<int>(threadIdx.x);
+      fetch(t < sw.lev[l + 2] ? t : -1, nxt);
+    }
+    if (cur.pos >= 0) solve(cur);
+    for (int t = b + static_cast<int>(threadIdx.x) + blockDim.x; t < e; t += blockDim.x) {  // wide levels
+      Pre p;
+      fetch(t, p);
+      solve(p);
+    }
+    __syncthreads();
+    cur = nxt;
+    nxt.pos = -1;
+  }
+}
+
+// z = (L L^T)^-1 r: forward sweep r -> z, backward sweep in place.
+template <int D>
+__global__ void __launch_bounds__(256) k_ic_apply(IcDev ic, const double* __restrict__ r, double* z) {
   const int c = blockIdx.x;
-  for (int l = 0; l < ic.nlf; ++l) {
-    for (int t = ic.flev[l] + threadIdx.x; t < ic.flev[l + 1]; t += blockDim.x) {
-      const int i = ic.frows[t];
-      const long pi = ic.pos[i];
-      double acc = r[pi * D + c];
-      const int b = ic.fptr[i], e = ic.fptr[i + 1] - 1;
-      for (int k = b; k < e; ++k) acc -= ic.fval[k] * z[static_cast<long>(ic.fcol[k]) * D + c];
-      z[pi * D + c] = acc / ic.fval[e];
-    }
-    __syncthreads();
-  }
-  for (int l = 0; l < ic.nlb; ++l) {
-    for (int t = ic.blev[l] + threadIdx.x; t < ic.blev[l + 1]; t += blockDim.x) {
-      const int j = ic.brows[t];
-      const long pj = ic.pos[j];
-      double acc = z[pj * D + c];
-      for (int k = ic.bptr[j]; k < ic.bptr[j + 1]; ++k) acc -= ic.bval[k] * z[static_cast<long>(ic.bcol[k]) * D + c];
-      z[pj * D + c] = acc / ic.bdg[j];
-    }
-    __syncthreads();
-  }
+  ic_sweep<D>(ic.fwd, r, z, c);
+  ic_sweep<D>(ic.bwd, z, z, c);
 }
 
 // tot[slot * D + j] = sum_v r_vj z_vj (pcg.cpp:66 / 85 with z = M^-1 r):
@@ -482,7 +520,7 @@ __global__ void __launch_bounds__(256) k_ic_dot(int n, const double* __restrict_
 
 template <int D>
 void ic_apply_d(const IcDev& ic, const double* r, double* z, cudaStream_t s) {
-  k_ic_apply<D><<<D, 1024, 0, s>>>(ic, r, z);
+  k_ic_apply<D><<<D, 256, 0, s>>>(ic, r, z);
 }
 template <int D>
 void ic_dot_d(int n, const double* r, const double* z, double* part, pfe_dev::Ctl* ctl, double* tot, int grid,
@@ -652,47 +690,72 @@ void build_ic(pfe_solver* S, int n, const std::vector<int>& aptr, const std::vec
   }
   std::vector<int> frows, flev;
   by_level(lev, nlf, frows, flev);
-  std::vector<int> fcol(f.idx.size());
-  for (size_t k = 0; k < f.idx.size(); ++k) fcol[k] = perm[f.idx[k]];
-  // backward: below-diagonal entries of column j, rows descending
+  // backward: below-diagonal entries of column j, rows descending; levels
+  // from the columns of L (a column waits for every row that updates it)
   std::vector<int> bptr(static_cast<size_t>(n) + 1, 0);
   for (int i = 0; i < n; ++i)
     for (int k = f.ptr[i]; k < f.ptr[i + 1] - 1; ++k) ++bptr[f.idx[k] + 1];
   for (int j = 0; j < n; ++j) bptr[j + 1] += bptr[j];
-  std::vector<int> bcol(static_cast<size_t>(bptr[n])), bfill(bptr.begin(), bptr.end() - 1);
-  std::vector<double> bval(static_cast<size_t>(bptr[n])), bdg(static_cast<size_t>(n));
+  std::vector<int> brow(static_cast<size_t>(bptr[n])), bfill(bptr.begin(), bptr.end() - 1);
+  std::vector<double> bval(static_cast<size_t>(bptr[n]));
   std::vector<int> blv(static_cast<size_t>(n), 0);
   int nlb = 0;
   for (int i = n - 1; i >= 0; --i) {
     nlb = std::max(nlb, blv[i] + 1);
     for (int k = f.ptr[i]; k < f.ptr[i + 1] - 1; ++k) {
       const int j = f.idx[k];
-      bcol[bfill[j]] = perm[i];
+      brow[bfill[j]] = i;
       bval[bfill[j]++] = f.val[k];
       blv[j] = std::max(blv[j], blv[i] + 1);
     }
   }
-  for (int j = 0; j < n; ++j) bdg[j] = f.val[f.ptr[j + 1] - 1];
   std::vector<int> brows, blev;
   by_level(blv, nlb, brows, blev);
+  // level-ordered slots with their entries laid out contiguously
   cudaStream_t st = S->stream;
-  IcDev& d = S->icd;
-  d.pos = S->mem.upload(perm, st);
-  d.fptr = S->mem.upload(f.ptr, st);
-  d.fcol = S->mem.upload(fcol, st);
-  d.fval = S->mem.upload(f.val, st);
-  d.frows = S->mem.upload(frows, st);
-  d.flev = S->mem.upload(flev, st);
-  d.nlf = nlf;
-  d.bptr = S->mem.upload(bptr, st);
-  d.bcol = S->mem.upload(bcol, st);
-  d.bval = S->mem.upload(bval, st);
-  d.bdg = S->mem.upload(bdg, st);
-  d.brows = S->mem.upload(brows, st);
-  d.blev = S->mem.upload(blev, st);
-  d.nlb = nlb;
+  auto upload_sweep = [&](const std::vector<int>& rows, const std::vector<int>& levs, int nl, auto&& row_entries,
+                          auto&& row_diag, IcSweep& out) {
+    std::vector<int> spos(static_cast<size_t>(n)), sbeg(static_cast<size_t>(n)), slen(static_cast<size_t>(n)), ecol;
+    std::vector<double> sdg(static_cast<size_t>(n)), ev;
+    for (int t = 0; t < n; ++t) {
+      const int i = rows[t];
+      spos[t] = perm[i];
+      sbeg[t] = static_cast<int>(ecol.size());
+      row_entries(i, ecol, ev);
+      slen[t] = static_cast<int>(ecol.size()) - sbeg[t];
+      sdg[t] = row_diag(i);
+    }
+    out.spos = S->mem.upload(spos, st);
+    out.sbeg = S->mem.upload(sbeg, st);
+    out.slen = S->mem.upload(slen, st);
+    out.sdg = S->mem.upload(sdg, st);
+    out.ecol = S->mem.upload(ecol, st);
+    out.eval = S->mem.upload(ev, st);
+    out.lev = S->mem.upload(levs, st);
+    out.nl = nl;
+    CK(cudaStreamSynchronize(st));  // the host vectors die here
+  };
+  // forward row i: L_ik, k < i, ascending columns (sparse.cpp:209-218)
+  upload_sweep(
+      frows, flev, nlf,
+      [&](int i, std::vector<int>& ec, std::vector<double>& ev) {
+        for (int k = f.ptr[i]; k < f.ptr[i + 1] - 1; ++k) {
+          ec.push_back(perm[f.idx[k]]);
+          ev.push_back(f.val[k]);
+        }
+      },
+      [&](int i) { return f.val[f.ptr[i + 1] - 1]; }, S->icd.fwd);
+  // backward column j: L_ij, i > j, descending rows (sparse.cpp:225-236)
+  upload_sweep(
+      brows, blev, nlb,
+      [&](int j, std::vector<int>& ec, std::vector<double>& ev) {
+        for (int k = bptr[j]; k < bptr[j + 1]; ++k) {
+          ec.push_back(perm[brow[k]]);
+          ev.push_back(bval[k]);
+        }
+      },
+      [&](int j) { return f.val[f.ptr[j + 1] - 1]; }, S->icd.bwd);
   S->zbuf = S->mem.alloc<double>(static_cast<size_t>(n) * S->d);
-  CK(cudaStreamSynchronize(st));  // host vectors die here
 }
 
 void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad) {
