@@ -500,6 +500,45 @@ inline Matrix random_embedding(int n, int d, std::uint64_t seed, const Vector& d
   return out;
 }
 
+// GMM initial embedding on the GPU (init.hpp: gmm_fit + init_embedding in
+// one call; pfe_gmm_init_device).  features: n x 3 (column-major, as the
+// reference's MatrixXd).  The fitted model is returned through `model`.
+struct GmmModel {
+  int k = 0;
+  Matrix means;      // k x 3
+  Matrix variances;  // k x 3, floored at 1e-6
+  Vector weights;    // simplex, length k
+};
+
+inline Matrix gmm_init_embedding(const Matrix& features, int k, std::uint64_t seed, const Vector& degrees,
+                                 GmmModel* model = nullptr, int device = 0) {
+  const long n = features.rows();
+  if (features.cols() != 3) throw ConfigError("gmm_fit: features must be n x 3");
+  if (degrees.size() != n) throw ConfigError("init_embedding: degree size mismatch");
+  std::vector<double> rgb(static_cast<size_t>(3 * n));
+  for (long i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) rgb[static_cast<size_t>(3 * i + c)] = features(i, c);
+  Matrix out = detail::make_matrix<Matrix>(n, k > 0 ? k : 1);
+  std::vector<double> means(static_cast<size_t>(3 * std::max(k, 1))), vars(means.size()),
+      wts(static_cast<size_t>(std::max(k, 1)));
+  detail::check(pfe_gmm_init_device(static_cast<int32_t>(n), rgb.data(), k, seed, degrees.data(), device, out.data(),
+                                    means.data(), vars.data(), wts.data()));
+  if (model) {
+    model->k = k;
+    model->means = detail::make_matrix<Matrix>(k, 3);
+    model->variances = detail::make_matrix<Matrix>(k, 3);
+    model->weights = Vector(static_cast<long>(k));
+    for (int j = 0; j < k; ++j) {
+      for (int c = 0; c < 3; ++c) {
+        model->means(j, c) = means[static_cast<size_t>(3 * j + c)];
+        model->variances(j, c) = vars[static_cast<size_t>(3 * j + c)];
+      }
+      model->weights[j] = wts[static_cast<size_t>(j)];
+    }
+  }
+  return out;
+}
+
 struct Segmentation {
   std::vector<int> labels;
   int k = 0;

@@ -160,5 +160,37 @@ int main() {
     CHECK(throws<pfe::ConfigError>([&] { pfe::PcgOperator(eye, bad); }));
   }
   std::printf("%s (%d failures)\n", failures ? "FACADE TEST FAILED" : "facade test passed", failures);
+  // GMM initial embedding (init.hpp: gmm_fit + init_embedding) on the GPU:
+  // Y0^T D Y0 = I, weights on the simplex, variances floored
+  {
+    std::mt19937_64 rng(3);
+    std::normal_distribution<double> nz(0.0, 0.03);
+    const int n = 600;
+    pfe::Matrix f(n, 3);
+    pfe::Vector deg(n);
+    for (int i = 0; i < n; ++i) {
+      const int q = i % 3;
+      for (int c = 0; c < 3; ++c) f(i, c) = (c == q ? 0.8 : 0.2) + nz(rng);
+      deg[i] = 1.0 + 0.01 * (i % 7);
+    }
+    pfe::GmmModel model;
+    pfe::Matrix y = pfe::gmm_init_embedding(f, 3, 0, deg, &model);
+    double dev = 0.0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += y(i, a) * deg[i] * y(i, b);
+        dev = std::max(dev, std::abs(acc - (a == b ? 1.0 : 0.0)));
+      }
+    CHECK(dev < 1e-10);
+    CHECK(model.k == 3);
+    double ws = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      ws += model.weights[j];
+      for (int c = 0; c < 3; ++c) CHECK(model.variances(j, c) >= 1e-6);
+    }
+    CHECK(std::abs(ws - 1.0) < 1e-12);
+    CHECK(throws<pfe::ConfigError>([&] { pfe::gmm_init_embedding(f, 0, 0, deg); }));
+  }
   return failures;
 }
