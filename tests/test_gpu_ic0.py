@@ -101,3 +101,46 @@ def test_ic0_standalone_split_bregman_matches_oracle():
     for a, c in zip(traj, exp_traj):
         assert np.abs(a - c).max() <= 1e-10
     assert np.abs(got - exp).max() <= 1e-10
+
+
+def test_ic0_breakdown_falls_back_to_jacobi_like_the_reference():
+    """A matrix without a stored diagonal entry in one row: IC(0) breaks
+    down for every shift, PcgOperator falls back to Jacobi and says so
+    (pcg.cpp:22-28) -- same iterations and result as the oracle."""
+    n = 6
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j in (i - 1, i, i + 1):
+            if 0 <= j < n and not (i == 3 and j == 3):
+                rows.append(i)
+                cols.append(j)
+                vals.append(4.0 if i == j else -1.0)
+    ptr = np.zeros(n + 1, np.int32)
+    np.add.at(ptr, np.array(rows) + 1, 1)
+    ptr = np.cumsum(ptr).astype(np.int32)
+    a = (ptr, np.array(cols, np.int32), np.array(vals))
+    rng = np.random.Generator(np.random.PCG64(4))
+    b, x0 = rng.normal(size=(n, 2)), np.zeros((n, 2))
+    x, reps = api.pcg_solve_multi(a, b, x0, api.PcgConfig(1e-8, 100, api.Preconditioner.Ic0))
+    xo, its, conv, _ = O.pcg_solve_multi(a, b, x0, 1e-8, 100, int(api.Preconditioner.Ic0))
+    assert all(r.jacobi_fallback for r in reps)
+    assert [r.iterations for r in reps] == list(its)
+    assert np.abs(x - xo).max() <= 1e-12 * max(1.0, np.abs(xo).max())
+
+
+def test_ic0_disconnected_graph_and_stage2():
+    """Two components, Stage II with conv_tol: the IC(0) path matches the
+    oracle's two_stage."""
+    rng = np.random.Generator(np.random.PCG64(8))
+    g1 = random_graph(30, 60, rng)
+    g2 = random_graph(25, 40, rng)
+    ei = np.concatenate([g1.ei, g2.ei + 30])
+    ej = np.concatenate([g1.ej, g2.ej + 30])
+    w = np.concatenate([g1.w, g2.w])
+    g = api.WeightedGraph(55, ei, ej, w, api.degree_vector(ei, ej, w, 55))
+    prm = ic0(3, lam=20.0, soc=2, sb=3, stage2=4, conv=1e-9)
+    y0 = api.random_embedding(g.n, 3, 1, g.degree)
+    s = api.PfeSolver(g, prm, warn=False)
+    got = s.two_stage(y0).y
+    exp = O.solve(g, prm, y0, mode=1)
+    assert rel_signed(got, exp) <= 1e-9
