@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -21,6 +22,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <utility>
 #include <vector>
@@ -100,6 +102,101 @@ void retain_pool_memory(int dev) {
   done[dev] = true;
 }
 
+// f(begin, end) over [0, n) on up to 16 host threads (chunks of >= grain
+// items; small inputs run inline).  f must not throw.
+template <class F>
+void parallel_for(long n, F&& f, long grain = 1L << 16) {
+  const long hw = std::max(1u, std::thread::hardware_concurrency());
+  const int t = static_cast<int>(std::min<long>(std::min<long>(hw, 16), (n + grain - 1) / std::max(1L, grain)));
+  if (t <= 1) {
+    f(0L, n);
+    return;
+  }
+  const long per = (n + t - 1) / t;
+  std::vector<std::thread> pool;
+  for (int w = 0; w < t; ++w) {
+    const long b = w * per, e = std::min(n, b + per);
+    if (b >= e) break;
+    pool.emplace_back([&f, b, e] { f(b, e); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Large copies between pageable host memory and the device go through two
+// process-wide 32 MB pinned bounce buffers, the host side of each chunk
+// copied by several threads (a pageable cudaMemcpy ran at ~2 GB/s, e.g.
+// 0.5 s to download C4's 1 GB embedding).
+struct PinnedStage {
+  std::mutex mu;
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  static constexpr size_t kCap = 32u << 20;
+  bool ok = false, tried = false;
+  bool ready() {
+    if (!tried) {
+      tried = true;
+      ok = cudaMallocHost(&buf[0], kCap) == cudaSuccess && cudaMallocHost(&buf[1], kCap) == cudaSuccess &&
+           cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) cudaGetLastError();
+    }
+    return ok;
+  }
+};
+PinnedStage& pinned_stage() {
+  static PinnedStage* s = new PinnedStage();  // never destroyed: no CUDA calls at exit
+  return *s;
+}
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  parallel_for(static_cast<long>(bytes), [&](long b, long e) {
+    std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, static_cast<size_t>(e - b));
+  }, 1L << 21);
+}
+constexpr size_t kStageMin = 16u << 20;  // smaller copies go direct
+
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  PinnedStage& ps = pinned_stage();
+  if (bytes < kStageMin || !ps.ready()) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  std::lock_guard<std::mutex> lk(ps.mu);
+  int i = 0;
+  for (size_t off = 0; off < bytes; off += PinnedStage::kCap, i ^= 1) {
+    const size_t n = std::min(PinnedStage::kCap, bytes - off);
+    CK(cudaEventSynchronize(ps.ev[i]));  // the previous copy out of this buffer is done
+    par_memcpy(ps.buf[i], static_cast<const char*>(src) + off, n);
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, ps.buf[i], n, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ps.ev[i], s));
+  }
+}
+
+// Blocking: returns when dst holds the data.
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  PinnedStage& ps = pinned_stage();
+  if (bytes < kStageMin || !ps.ready()) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  std::lock_guard<std::mutex> lk(ps.mu);
+  const size_t cap = PinnedStage::kCap;
+  const size_t nchunks = (bytes + cap - 1) / cap;
+  auto issue = [&](size_t c) {
+    const size_t off = c * cap, n = std::min(cap, bytes - off);
+    CK(cudaMemcpyAsync(ps.buf[c & 1], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ps.ev[c & 1], s));
+  };
+  issue(0);
+  if (nchunks > 1) issue(1);
+  for (size_t c = 0; c < nchunks; ++c) {
+    CK(cudaEventSynchronize(ps.ev[c & 1]));
+    const size_t off = c * cap, n = std::min(cap, bytes - off);
+    par_memcpy(static_cast<char*>(dst) + off, ps.buf[c & 1], n);
+    if (c + 2 < nchunks) issue(c + 2);
+  }
+}
+
 // Process-wide pool of pinned host control blocks: cudaMallocHost /
 // cudaFreeHost cost milliseconds each (cudaFreeHost synchronizes the
 // device), which showed up as ~7 ms per pfe_solve call on small graphs.
@@ -146,7 +243,7 @@ struct DevPool {
   template <class T>
   T* upload(const std::vector<T>& v, cudaStream_t s) {
     T* d = alloc<T>(v.size());
-    if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (!v.empty()) copy_h2d(d, v.data(), v.size() * sizeof(T), s);
     return d;
   }
   void release(void* p) {
@@ -553,7 +650,21 @@ struct HostGraph {
 void validate(const HostGraph& g, const pfe_params& p, bool check_solver_caps) {
   if (g.n < 1) config_error("graph: n must be >= 1");
   if (g.m < 0) config_error("graph: negative edge count");
-  for (long k = 0; k < g.m; ++k) {
+  // first offending edge found in parallel, then reported by the serial
+  // checks below in the reference's order
+  std::atomic<long> first_bad{g.m};
+  parallel_for(g.m, [&](long b, long e) {
+    for (long k = b; k < e; ++k) {
+      const int i = g.ei[k], j = g.ej[k];
+      if (i < 0 || i >= g.n || j < 0 || j >= g.n || !std::isfinite(g.w[k]) || i >= j) {
+        long cur = first_bad.load();
+        while (k < cur && !first_bad.compare_exchange_weak(cur, k)) {
+        }
+        return;
+      }
+    }
+  });
+  for (long k = first_bad.load(); k < g.m; ++k) {
     const int i = g.ei[k], j = g.ej[k];
     if (i < 0 || i >= g.n || j < 0 || j >= g.n)
       config_error("csr_from_triplets: entry (" + std::to_string(k) + "," + std::to_string(i < 0 || i >= g.n ? i : j) +
@@ -767,10 +878,12 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
 
   auto finish_diag = [&](std::vector<double>& diag) {
     std::vector<double> invd(n);
-    for (int v = 0; v < n; ++v) {
-      diag[v] += dterm * g.deg[v];  // the (r/2) d_v triplet is summed last
-      invd[v] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[v] > 0.0 ? 1.0 / diag[v] : 1.0);
-    }
+    parallel_for(n, [&](long b, long e) {
+      for (long v = b; v < e; ++v) {
+        diag[v] += dterm * g.deg[v];  // the (r/2) d_v triplet is summed last
+        invd[v] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[v] > 0.0 ? 1.0 / diag[v] : 1.0);
+      }
+    });
     S->diag = S->mem.upload(diag, st);
     S->invd = S->mem.upload(invd, st);
   };
@@ -784,11 +897,16 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     slot_of.resize(static_cast<size_t>(m));
     const int S_ = grad == 1 ? 4 : 12;
     // j - i identifies (dy, dx) uniquely since |dx| <= R < W / 2; the column
-    // of i (tracked incrementally: edges are sorted by i) rules out wrap-around
+    // of i rules out wrap-around
+    std::atomic<bool> ok{true};
+    parallel_for(m, [&](long kb, long ke) {
     int cur_i = -1, xi = 0;
-    for (long k = 0; k < m && grid; ++k) {
+    for (long k = kb; k < ke; ++k) {
       const int i = g.ei[k], j = g.ej[k];
-      if (k > 0 && !(g.ei[k - 1] < i || (g.ei[k - 1] == i && g.ej[k - 1] < j))) grid = false;
+      if (k > 0 && !(g.ei[k - 1] < i || (g.ei[k - 1] == i && g.ej[k - 1] < j))) {
+        ok = false;
+        return;
+      }
       if (i != cur_i) {
         xi = i % gw;
         cur_i = i;
@@ -807,9 +925,14 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
           else if (dy == 2 && dx >= -2 && dx <= 2) s = 9 + dx;
         }
       }
-      if (s < 0) grid = false;
+      if (s < 0) {
+        ok = false;
+        return;
+      }
       slot_of[k] = static_cast<long>(i) * S_ + s;
     }
+    });
+    grid = ok.load();
   }
   if (grid) {
     const int S_ = grad == 1 ? 4 : 12;
@@ -818,7 +941,9 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       S->row_hi = gh;
     }
     std::vector<double> wf(static_cast<size_t>(n) * S_, 0.0);
-    for (long k = 0; k < m; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
+    parallel_for(m, [&](long b, long e) {
+      for (long k = b; k < e; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
+    });
     // diag(A)_v: incident edges in edge-index order = backward slots (u
     // ascending) then forward slots; absent slots hold 0 and add +0.0.
     std::vector<double> diag(n, 0.0);
@@ -828,7 +953,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       sdx[s] = grad == 1 ? (s == 0 ? 1 : s - 2) : (s < 2 ? s + 1 : (s < 7 ? s - 4 : s - 9));
       off[s] = sdy[s] * gw + sdx[s];
     }
-    for (int y = 0, v = 0; y < gh; ++y) {
+    parallel_for(gh, [&](long yb, long ye) {
+    for (int y = static_cast<int>(yb), v = static_cast<int>(yb) * gw; y < ye; ++y) {
       for (int x = 0; x < gw; ++x, ++v) {
         double acc = 0.0;
         for (int s = S_ - 1; s >= 0; --s) {
@@ -844,6 +970,7 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
         diag[v] = acc;
       }
     }
+    }, std::max(1L, (1L << 16) / gw));
     finish_diag(diag);
     double* dwf = S->mem.upload(wf, st);
     S->edge_row = std::move(slot_of);
@@ -1102,7 +1229,7 @@ __global__ void k_scale_rows(long n, int d, const double* __restrict__ s, const 
 
 // host col-major n x d -> device row-major via a staging buffer
 void upload_rows(pfe_solver* S, const double* host, long n, int d, double* dst, double* staging) {
-  CK(cudaMemcpyAsync(staging, host, sizeof(double) * n * d, cudaMemcpyHostToDevice, S->stream));
+  copy_h2d(staging, host, sizeof(double) * n * d, S->stream);
   k_colmajor_to_rows<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, staging, dst,
                                                                              n == S->n ? S->perm_d : nullptr);
   CK(cudaGetLastError());
@@ -1111,8 +1238,7 @@ void download_rows(pfe_solver* S, const double* src, long n, int d, double* host
   k_rows_to_colmajor<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, src, staging,
                                                                              n == S->n ? S->perm_d : nullptr);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(host, staging, sizeof(double) * n * d, cudaMemcpyDeviceToHost, S->stream));
-  CK(cudaStreamSynchronize(S->stream));
+  copy_d2h(host, staging, sizeof(double) * n * d, S->stream);
 }
 
 void state_init_from_y0(pfe_state* st) {
