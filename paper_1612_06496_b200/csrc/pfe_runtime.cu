@@ -1016,35 +1016,54 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
 
   // General CSR: A rows sorted by column with duplicate columns summed in
-  // edge order (stable sort), exact zeros dropped, diagonal in place.
-  std::vector<int> aptr(static_cast<size_t>(n) + 1, 0), acol;
-  std::vector<double> aval;
-  acol.reserve(static_cast<size_t>(2 * m + n));
-  aval.reserve(static_cast<size_t>(2 * m + n));
-  std::vector<std::pair<int, double>> row;
+  // edge order (stable sort), exact zeros dropped, diagonal in place.  Rows
+  // are merged in parallel into an upper-bound layout, then compacted.
+  std::vector<long> ub(static_cast<size_t>(n) + 1, 0);
   for (int x = 0; x < n; ++x) {
-    const int v = inv[x];  // storage row x holds vertex v's row, in the reference's column order
-    row.clear();
-    for (int k = iptr[v]; k < iptr[v + 1]; ++k) row.emplace_back(inbr[k], -((hl * iw[k]) * iw[k]));
-    row.emplace_back(v, diag[v]);
-    std::stable_sort(row.begin(), row.end(),
-                     [](const std::pair<int, double>& a, const std::pair<int, double>& b) { return a.first < b.first; });
-    for (size_t t = 0; t < row.size();) {
-      const int col = row[t].first;
-      double s = 0.0;
-      if (col == v) {
-        s = row[t].second;  // diagonal already accumulated in csr_from_triplets order
-        ++t;
-      } else {
-        for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
-      }
-      if (s != 0.0) {
-        acol.push_back(perm[col]);
-        aval.push_back(s);
-      }
-    }
-    aptr[x + 1] = static_cast<int>(acol.size());
+    const int v = inv[x];
+    ub[x + 1] = ub[x] + (iptr[v + 1] - iptr[v]) + 1;
   }
+  std::vector<int> tcol(static_cast<size_t>(ub[n])), tlen(static_cast<size_t>(n));
+  std::vector<double> tval(static_cast<size_t>(ub[n]));
+  parallel_for(n, [&](long xb, long xe) {
+    std::vector<std::pair<int, double>> row;
+    for (long x = xb; x < xe; ++x) {
+      const int v = inv[x];  // storage row x holds vertex v's row, in the reference's column order
+      row.clear();
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k) row.emplace_back(inbr[k], -((hl * iw[k]) * iw[k]));
+      row.emplace_back(v, diag[v]);
+      std::stable_sort(row.begin(), row.end(),
+                       [](const std::pair<int, double>& a, const std::pair<int, double>& b) { return a.first < b.first; });
+      long at = ub[x];
+      for (size_t t = 0; t < row.size();) {
+        const int col = row[t].first;
+        double s = 0.0;
+        if (col == v) {
+          s = row[t].second;  // diagonal already accumulated in csr_from_triplets order
+          ++t;
+        } else {
+          for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
+        }
+        if (s != 0.0) {
+          tcol[static_cast<size_t>(at)] = perm[col];
+          tval[static_cast<size_t>(at)] = s;
+          ++at;
+        }
+      }
+      tlen[x] = static_cast<int>(at - ub[x]);
+    }
+  }, 4096);
+  std::vector<int> aptr(static_cast<size_t>(n) + 1, 0);
+  for (int x = 0; x < n; ++x) aptr[x + 1] = aptr[x] + tlen[x];
+  std::vector<int> acol(static_cast<size_t>(aptr[n]));
+  std::vector<double> aval(static_cast<size_t>(aptr[n]));
+  parallel_for(n, [&](long xb, long xe) {
+    for (long x = xb; x < xe; ++x) {
+      std::copy(tcol.begin() + ub[x], tcol.begin() + ub[x] + tlen[x], acol.begin() + aptr[x]);
+      std::copy(tval.begin() + ub[x], tval.begin() + ub[x] + tlen[x], aval.begin() + aptr[x]);
+    }
+  }, 4096);
+  std::vector<std::pair<int, double>> row;
   if (S->ic) {
     // A in the reference's row order (the IC(0) factor depends on it)
     std::vector<int> nptr(static_cast<size_t>(n) + 1, 0), ncol;
@@ -1078,25 +1097,41 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   // edge storage follows the vertex storage order: the edges a vertex owns
   // (it is their first endpoint) are consecutive rows of the edge arrays
   std::vector<int> epos(static_cast<size_t>(m));
-  for (int x = 0, next = 0; x < n; ++x) {
+  std::vector<int> own(static_cast<size_t>(n) + 1, 0);  // owned-edge offsets in storage order
+  for (int x = 0; x < n; ++x) {
     const int v = inv[x];
-    for (int k = iptr[v]; k < iptr[v + 1]; ++k)
-      if (inbr[k] > v) epos[ieid[k]] = next++;
+    int c = 0;
+    for (int k = iptr[v]; k < iptr[v + 1]; ++k) c += inbr[k] > v ? 1 : 0;
+    own[x + 1] = own[x] + c;
   }
+  parallel_for(n, [&](long xb, long xe) {
+    for (long x = xb; x < xe; ++x) {
+      const int v = inv[x];
+      int next = own[x];
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k)
+        if (inbr[k] > v) epos[ieid[k]] = next++;
+    }
+  }, 4096);
   // incidence lists in storage order: (neighbour row, w, edge row << 1 | [v is
   // the edge's first endpoint]), each in increasing edge index
   std::vector<int> iptr2(static_cast<size_t>(n) + 1, 0), inbr2(static_cast<size_t>(2 * m)),
       ieid2(static_cast<size_t>(2 * m));
   std::vector<double> iw2(static_cast<size_t>(2 * m));
-  for (int x = 0, at = 0; x < n; ++x) {
+  for (int x = 0; x < n; ++x) {
     const int v = inv[x];
-    for (int k = iptr[v]; k < iptr[v + 1]; ++k, ++at) {
-      inbr2[at] = perm[inbr[k]];
-      ieid2[at] = (epos[ieid[k]] << 1) | (inbr[k] > v ? 1 : 0);
-      iw2[at] = iw[k];
-    }
-    iptr2[x + 1] = at;
+    iptr2[x + 1] = iptr2[x] + (iptr[v + 1] - iptr[v]);
   }
+  parallel_for(n, [&](long xb, long xe) {
+    for (long x = xb; x < xe; ++x) {
+      const int v = inv[x];
+      int at = iptr2[x];
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k, ++at) {
+        inbr2[at] = perm[inbr[k]];
+        ieid2[at] = (epos[ieid[k]] << 1) | (inbr[k] > v ? 1 : 0);
+        iw2[at] = iw[k];
+      }
+    }
+  }, 4096);
   S->perm_h = perm;
   S->perm_d = S->mem.upload(perm, st);
   S->edge_row.assign(epos.begin(), epos.end());
