@@ -1224,14 +1224,22 @@ pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exe
   }
   S->n = g->n;
   S->m = g->m;
+  const auto t1 = std::chrono::steady_clock::now();
   build_topology(S.get(), hg, S->ic ? 0 : g->grid_h, S->ic ? 0 : g->grid_w, S->ic ? 0 : g->grid_radius);
+  const auto t2 = std::chrono::steady_clock::now();
   upload_degree(S.get(), g->degree);
   S->qr_blocks = qr_blocks_for(S.get(), g->n);
   S->rbuf = S->mem.alloc<double>(static_cast<size_t>(S->qr_blocks) * S->d * S->d);
   S->wmat = S->mem.alloc<double>(static_cast<size_t>(S->d) * S->d);
   S->ensure_log(64);
   CK(cudaStreamSynchronize(S->stream));
-  S->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const auto t3 = std::chrono::steady_clock::now();
+  S->setup_s = std::chrono::duration<double>(t3 - t0).count();
+  if (const char* e = std::getenv("PFE_SETUP_TIMING"); e && e[0] == '1') {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "pfe_solver_create: validate + init %.2f ms, topology %.2f ms, degree + sync %.2f ms\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
   return S.release();
 }
 
