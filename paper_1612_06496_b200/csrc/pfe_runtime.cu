@@ -143,9 +143,13 @@ struct PinnedStage {
     return ok;
   }
 };
+// One stage per device: its events belong to that device's streams (a
+// multi-GPU solve drives several devices from one process).
 PinnedStage& pinned_stage() {
-  static PinnedStage* s = new PinnedStage();  // never destroyed: no CUDA calls at exit
-  return *s;
+  static PinnedStage* stages = new PinnedStage[64];  // never destroyed: no CUDA calls at exit
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return stages[dev >= 0 && dev < 64 ? dev : 0];
 }
 void par_memcpy(void* dst, const void* src, size_t bytes) {
   parallel_for(static_cast<long>(bytes), [&](long b, long e) {
