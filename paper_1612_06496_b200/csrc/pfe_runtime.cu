@@ -741,26 +741,58 @@ Incidence build_incidence(const HostGraph& g) {
   const int n = g.n;
   const long m = g.m;
   c.iptr.assign(static_cast<size_t>(n) + 1, 0);
-  for (long k = 0; k < m; ++k) {
-    ++c.iptr[g.ei[k] + 1];
-    ++c.iptr[g.ej[k] + 1];
-  }
-  for (int v = 0; v < n; ++v) c.iptr[v + 1] += c.iptr[v];
   c.inbr.resize(static_cast<size_t>(2 * m));
   c.ieid.resize(static_cast<size_t>(2 * m));
   c.iw.resize(static_cast<size_t>(2 * m));
-  std::vector<int> fill(c.iptr.begin(), c.iptr.end() - 1);
-  for (long k = 0; k < m; ++k) {
-    const int i = g.ei[k], j = g.ej[k];
-    int at = fill[i]++;
-    c.inbr[at] = j;
-    c.ieid[at] = static_cast<int>(k);
-    c.iw[at] = g.w[k];
-    at = fill[j]++;
-    c.inbr[at] = i;
-    c.ieid[at] = static_cast<int>(k);
-    c.iw[at] = g.w[k];
+  // counting sort by vertex, edges kept in increasing index: T threads own
+  // consecutive edge chunks; per-thread counts give each thread its slots
+  const long hw = std::max(1u, std::thread::hardware_concurrency());
+  long T = std::min<long>(std::min<long>(hw, 16), std::max(1L, m / (1L << 18)));
+  T = std::max(1L, std::min<long>(T, (256L << 20) / (4L * std::max(1, n))));  // counts memory cap
+  const long per = (m + T - 1) / T;
+  std::vector<int> cnt(static_cast<size_t>(T) * n, 0);
+  auto run = [&](auto&& body) {
+    std::vector<std::thread> pool;
+    for (long t = 0; t < T; ++t) pool.emplace_back([&, t] { body(t, t * per, std::min(m, (t + 1) * per)); });
+    for (auto& th : pool) th.join();
+  };
+  run([&](long t, long kb, long ke) {
+    int* ct = cnt.data() + t * n;
+    for (long k = kb; k < ke; ++k) {
+      ++ct[g.ei[k]];
+      ++ct[g.ej[k]];
+    }
+  });
+  for (int v = 0; v < n; ++v) {
+    int tot = 0;
+    for (long t = 0; t < T; ++t) tot += cnt[static_cast<size_t>(t) * n + v];
+    c.iptr[v + 1] = c.iptr[v] + tot;
   }
+  parallel_for(n, [&](long vb, long ve) {  // counts -> each thread's first slot per vertex
+    for (long v = vb; v < ve; ++v) {
+      int base = c.iptr[v];
+      for (long t = 0; t < T; ++t) {
+        int& x = cnt[static_cast<size_t>(t) * n + v];
+        const int k = x;
+        x = base;
+        base += k;
+      }
+    }
+  });
+  run([&](long t, long kb, long ke) {
+    int* fill = cnt.data() + t * n;
+    for (long k = kb; k < ke; ++k) {
+      const int i = g.ei[k], j = g.ej[k];
+      int at = fill[i]++;
+      c.inbr[at] = j;
+      c.ieid[at] = static_cast<int>(k);
+      c.iw[at] = g.w[k];
+      at = fill[j]++;
+      c.inbr[at] = i;
+      c.ieid[at] = static_cast<int>(k);
+      c.iw[at] = g.w[k];
+    }
+  });
   return c;
 }
 
