@@ -548,7 +548,7 @@ pfe_solver* create_range_solver(const pfe_graph* g, const pfe_params* p, const p
   const int n = g->n, P = nranks, d = S->d;
   const double hl = 0.5 * S->prm.lambda, dterm = 0.5 * S->prm.r;
   const Incidence inc = build_incidence(hg);
-  const std::vector<int> pos = bfs_storage_order(n, inc.iptr, inc.inbr);
+  const std::vector<int> pos = bfs_storage_order(n, inc.iptr, inc.inbr.data());
   std::vector<int> vat(n);
   for (int v = 0; v < n; ++v) vat[pos[v]] = v;
   S->range_vertex = vat;

@@ -230,6 +230,30 @@ PinnedCtlPool& pinned_ctl_pool() {
   return *pool;
 }
 
+// std::vector whose elements are left uninitialised on resize (PODs that
+// are written before they are read): big set-up buffers are then not
+// zero-filled serially before the parallel loops fill them.
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = UninitAlloc<U>;
+  };
+  UninitAlloc() = default;
+  template <class U>
+  UninitAlloc(const UninitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using uvec = std::vector<T, UninitAlloc<T>>;
+
 struct DevPool {
   std::vector<void*> ptrs;
   cudaStream_t stream = nullptr;   // allocation stream, set before the first allocation
@@ -244,8 +268,8 @@ struct DevPool {
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
-  template <class T>
-  T* upload(const std::vector<T>& v, cudaStream_t s) {
+  template <class T, class A>
+  T* upload(const std::vector<T, A>& v, cudaStream_t s) {
     T* d = alloc<T>(v.size());
     if (!v.empty()) copy_h2d(d, v.data(), v.size() * sizeof(T), s);
     return d;
@@ -710,7 +734,7 @@ int grid_slot(int R, int W, int i, int j) {
 // Breadth-first order of the vertices (components in vertex order, neighbours
 // in incidence order): perm[v] = position of v.  Used as the storage order of
 // general graphs and as the basis of vertex-range partitions.
-std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const std::vector<int>& inbr) {
+std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const int* inbr) {
   std::vector<int> perm(n, -1), queue(n);
   int next = 0, head = 0;
   for (int s0 = 0; s0 < n; ++s0) {
@@ -733,8 +757,9 @@ std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const st
 
 // Incidence lists in increasing edge index (the row order of M^T).
 struct Incidence {
-  std::vector<int> iptr, inbr, ieid;
-  std::vector<double> iw;
+  std::vector<int> iptr;
+  uvec<int> inbr, ieid;
+  uvec<double> iw;
 };
 Incidence build_incidence(const HostGraph& g) {
   Incidence c;
@@ -1025,11 +1050,23 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
 
   // incidence lists in increasing edge index (the row order of M^T)
+  const bool tmr = [] {
+    const char* e = std::getenv("PFE_SETUP_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto tq = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!tmr) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  topology %-10s %.2f ms\n", what, std::chrono::duration<double, std::milli>(t - tq).count());
+    tq = t;
+  };
   Incidence inc = build_incidence(g);
+  mark("incidence");
   const std::vector<int>& iptr = inc.iptr;
-  const std::vector<int>& inbr = inc.inbr;
-  const std::vector<int>& ieid = inc.ieid;
-  const std::vector<double>& iw = inc.iw;
+  const uvec<int>& inbr = inc.inbr;
+  const uvec<int>& ieid = inc.ieid;
+  const uvec<double>& iw = inc.iw;
   std::vector<double> diag(n);
   for (int v = 0; v < n; ++v) {
     double acc = 0.0;
@@ -1038,7 +1075,9 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
   // storage order: BFS over the incidence graph (components in vertex order),
   // so the rows a vertex gathers sit near its own and stay in L2 / L1
-  std::vector<int> perm = bfs_storage_order(n, iptr, inbr), inv(n);
+  mark("diag");
+  std::vector<int> perm = bfs_storage_order(n, iptr, inbr.data()), inv(n);
+  mark("bfs");
   for (int v = 0; v < n; ++v) inv[perm[v]] = v;
   {
     // diag / inv_diag in storage order ((r/2) d_v is added last, as finish_diag does)
@@ -1059,8 +1098,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     const int v = inv[x];
     ub[x + 1] = ub[x] + (iptr[v + 1] - iptr[v]) + 1;
   }
-  std::vector<int> tcol(static_cast<size_t>(ub[n])), tlen(static_cast<size_t>(n));
-  std::vector<double> tval(static_cast<size_t>(ub[n]));
+  uvec<int> tcol(static_cast<size_t>(ub[n])), tlen(static_cast<size_t>(n));
+  uvec<double> tval(static_cast<size_t>(ub[n]));
   parallel_for(n, [&](long xb, long xe) {
     std::vector<std::pair<int, double>> row;
     for (long x = xb; x < xe; ++x) {
@@ -1089,10 +1128,11 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       tlen[x] = static_cast<int>(at - ub[x]);
     }
   }, 4096);
+  mark("rows");
   std::vector<int> aptr(static_cast<size_t>(n) + 1, 0);
   for (int x = 0; x < n; ++x) aptr[x + 1] = aptr[x] + tlen[x];
-  std::vector<int> acol(static_cast<size_t>(aptr[n]));
-  std::vector<double> aval(static_cast<size_t>(aptr[n]));
+  uvec<int> acol(static_cast<size_t>(aptr[n]));
+  uvec<double> aval(static_cast<size_t>(aptr[n]));
   parallel_for(n, [&](long xb, long xe) {
     for (long x = xb; x < xe; ++x) {
       std::copy(tcol.begin() + ub[x], tcol.begin() + ub[x] + tlen[x], acol.begin() + aptr[x]);
@@ -1132,7 +1172,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }
   // edge storage follows the vertex storage order: the edges a vertex owns
   // (it is their first endpoint) are consecutive rows of the edge arrays
-  std::vector<int> epos(static_cast<size_t>(m));
+  mark("compact");
+  uvec<int> epos(static_cast<size_t>(m));
   std::vector<int> own(static_cast<size_t>(n) + 1, 0);  // owned-edge offsets in storage order
   for (int x = 0; x < n; ++x) {
     const int v = inv[x];
@@ -1150,9 +1191,9 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   }, 4096);
   // incidence lists in storage order: (neighbour row, w, edge row << 1 | [v is
   // the edge's first endpoint]), each in increasing edge index
-  std::vector<int> iptr2(static_cast<size_t>(n) + 1, 0), inbr2(static_cast<size_t>(2 * m)),
-      ieid2(static_cast<size_t>(2 * m));
-  std::vector<double> iw2(static_cast<size_t>(2 * m));
+  std::vector<int> iptr2(static_cast<size_t>(n) + 1, 0);
+  uvec<int> inbr2(static_cast<size_t>(2 * m)), ieid2(static_cast<size_t>(2 * m));
+  uvec<double> iw2(static_cast<size_t>(2 * m));
   for (int x = 0; x < n; ++x) {
     const int v = inv[x];
     iptr2[x + 1] = iptr2[x] + (iptr[v + 1] - iptr[v]);
@@ -1168,6 +1209,7 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       }
     }
   }, 4096);
+  mark("remap");
   S->perm_h = perm;
   S->perm_d = S->mem.upload(perm, st);
   S->edge_row.assign(epos.begin(), epos.end());
@@ -1186,6 +1228,7 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   c.invd = S->invd;
   S->topo.kind = pfe_host::kTopoCsr;
   S->topo.csr = c;
+  mark("upload");
 }
 
 void init_common(pfe_solver* S, const pfe_exec* x, int d) {
