@@ -1068,11 +1068,13 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   const uvec<int>& ieid = inc.ieid;
   const uvec<double>& iw = inc.iw;
   std::vector<double> diag(n);
-  for (int v = 0; v < n; ++v) {
-    double acc = 0.0;
-    for (int k = iptr[v]; k < iptr[v + 1]; ++k) acc += (hl * iw[k]) * iw[k];
-    diag[v] = acc;
-  }
+  parallel_for(n, [&](long vb, long ve) {
+    for (long v = vb; v < ve; ++v) {
+      double acc = 0.0;
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k) acc += (hl * iw[k]) * iw[k];
+      diag[v] = acc;
+    }
+  }, 4096);
   // storage order: BFS over the incidence graph (components in vertex order),
   // so the rows a vertex gathers sit near its own and stay in L2 / L1
   mark("diag");
@@ -1175,12 +1177,15 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   mark("compact");
   uvec<int> epos(static_cast<size_t>(m));
   std::vector<int> own(static_cast<size_t>(n) + 1, 0);  // owned-edge offsets in storage order
-  for (int x = 0; x < n; ++x) {
-    const int v = inv[x];
-    int c = 0;
-    for (int k = iptr[v]; k < iptr[v + 1]; ++k) c += inbr[k] > v ? 1 : 0;
-    own[x + 1] = own[x] + c;
-  }
+  parallel_for(n, [&](long xb, long xe) {
+    for (long x = xb; x < xe; ++x) {
+      const int v = inv[x];
+      int c = 0;
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k) c += inbr[k] > v ? 1 : 0;
+      own[x + 1] = c;
+    }
+  }, 4096);
+  for (int x = 0; x < n; ++x) own[x + 1] += own[x];
   parallel_for(n, [&](long xb, long xe) {
     for (long x = xb; x < xe; ++x) {
       const int v = inv[x];
