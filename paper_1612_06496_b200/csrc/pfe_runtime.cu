@@ -1001,7 +1001,8 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       S->row_lo = 0;
       S->row_hi = gh;
     }
-    std::vector<double> wf(static_cast<size_t>(n) * S_, 0.0);
+    uvec<double> wf(static_cast<size_t>(n) * S_);  // zero-filled in parallel: absent slots stay 0
+    parallel_for(static_cast<long>(wf.size()), [&](long b, long e) { std::fill(wf.begin() + b, wf.begin() + e, 0.0); });
     parallel_for(m, [&](long b, long e) {
       for (long k = b; k < e; ++k) wf[static_cast<size_t>(slot_of[k])] = g.w[k];
     });
