@@ -208,6 +208,12 @@ int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_id
                         int32_t preconditioner, const pfe_exec* x, double* x_out, int32_t* iterations,
                         int32_t* converged, double* residual, int32_t* jacobi_fallback);
 
+/* The IC(0) breakdown test of the PcgOperator constructor (pcg.cpp:22-28):
+ * factors the CSR matrix on the host exactly as incomplete_cholesky does
+ * (sparse.cpp:124-203, up to 8 diagonal shifts) and sets *jacobi_fallback
+ * to 1 if the breakdown persisted.  Host only (no device needed). */
+int pfe_ic0_probe(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, const double* values,
+                  int32_t* jacobi_fallback);
 /* Multi-GPU row bands for pixel-grid graphs: one process
  * per GPU; rank 0 calls pfe_nccl_unique_id and shares the bytes (e.g. via
  * torch.distributed), then every rank creates its band solver from the SAME

@@ -3,6 +3,7 @@
 // ctypes.  Status codes follow proj/tools/main.cpp:431-446:
 // 0 ok, 1 IoError, 2 NumericalError, 3 ConfigError, 4 other.
 // Dense matrices are column-major (the reference's Eigen layout).
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -74,6 +75,10 @@ struct orc_params {
   int preconditioner;  // 0 Ic0, 1 Jacobi, 2 None
 };
 
+int orc_solve_timed(int mode, int n, int m, const int* ei, const int* ej, const double* w, const double* deg,
+                    const orc_params* prm, const double* y0, double* y_out, double* p_out, double* breg_out,
+                    double* sb_out, double* ss_out, int* pcg_log, int log_cap, long* n_inner, double* times);
+
 static Params to_params(const orc_params* p) {
   Params q;
   q.dim = p->dim;
@@ -107,13 +112,24 @@ int orc_d_orthonormalize(int n, int d, const double* a, const double* deg, doubl
 int orc_solve(int mode, int n, int m, const int* ei, const int* ej, const double* w, const double* deg,
               const orc_params* prm, const double* y0, double* y_out, double* p_out, double* breg_out,
               double* sb_out, double* ss_out, int* pcg_log, int log_cap, long* n_inner) {
+  return orc_solve_timed(mode, n, m, ei, ej, w, deg, prm, y0, y_out, p_out, breg_out, sb_out, ss_out, pcg_log,
+                         log_cap, n_inner, nullptr);
+}
+
+// orc_solve plus wall seconds {set-up, inner iterations, projections} in
+// times[0..2] (bench.py's CPU baseline times the inner loop only).
+int orc_solve_timed(int mode, int n, int m, const int* ei, const int* ej, const double* w, const double* deg,
+                    const orc_params* prm, const double* y0, double* y_out, double* p_out, double* breg_out,
+                    double* sb_out, double* ss_out, int* pcg_log, int log_cap, long* n_inner, double* times) {
   return guard([&] {
     Graph g = make_graph(n, m, ei, ej, w, deg);
     Params params = to_params(prm);
-    PfeSolver s(g, params);
     RunLog log;
+    const auto t0 = std::chrono::steady_clock::now();
+    PfeSolver s(g, params);
     s.log = &log;
     State st = s.make_state(make_mat(n, params.dim, y0));
+    log.t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     s.run_soc(st, params.soc_max, params.sb_max_stage1);
     if (mode == 1 && params.sb_max_stage2 > 0) s.split_bregman(st, params.sb_max_stage2);
     put(st.y, y_out);
@@ -124,8 +140,73 @@ int orc_solve(int mode, int n, int m, const int* ei, const int* ej, const double
     if (pcg_log)
       for (int i = 0; i < log_cap && i < static_cast<int>(log.pcg_iters.size()); ++i) pcg_log[i] = log.pcg_iters[i];
     if (n_inner) *n_inner = log.inner_iterations;
+    if (times) {
+      times[0] = log.t_setup;
+      times[1] = log.t_inner;
+      times[2] = log.t_outer;
+    }
   });
 }
+
+// A resident oracle solve for bench.py's CPU legs: the solver and state are
+// built once (orc_session_create, set-up seconds reported), then each
+// orc_session_step runs the next `inner` inner iterations of the soc
+// schedule (solver.cpp:110-126: b = s = 0 at the start of an outer
+// iteration, the projection after its sb_max-th inner iteration), so a
+// bounded sample of steps walks the same trajectory the full run does.
+struct orc_session {
+  PfeSolver solver;
+  State st;
+  RunLog log;
+  int sb_max = 1;
+  long pos = 0;  // inner iterations run so far
+  orc_session(const Graph& g, const Params& p) : solver(g, p), sb_max(p.sb_max_stage1) {}
+};
+
+int orc_session_create(int n, int m, const int* ei, const int* ej, const double* w, const double* deg,
+                       const orc_params* prm, const double* y0, orc_session** out, double* setup_s) {
+  return guard([&] {
+    Graph g = make_graph(n, m, ei, ej, w, deg);
+    Params params = to_params(prm);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto* ss = new orc_session(g, params);
+    ss->solver.log = &ss->log;
+    try {
+      ss->st = ss->solver.make_state(make_mat(n, params.dim, y0));
+    } catch (...) {
+      delete ss;
+      throw;
+    }
+    if (setup_s) *setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = ss;
+  });
+}
+
+// times[0] = inner-iteration seconds, times[1] = projection seconds of this
+// call; pcg_max[i] = PCG iterations (max over columns) of its i-th inner iteration.
+int orc_session_step(orc_session* ss, int inner, double* times, int* pcg_max) {
+  return guard([&] {
+    const double ti = ss->log.t_inner, to = ss->log.t_outer;
+    const size_t before = ss->log.pcg_iters.size();
+    for (int k = 0; k < inner; ++k) {
+      if (ss->pos % ss->sb_max == 0) {
+        std::fill(ss->st.split_b.a.begin(), ss->st.split_b.a.end(), 0.0);
+        std::fill(ss->st.split_s.a.begin(), ss->st.split_s.a.end(), 0.0);
+      }
+      ss->solver.split_bregman(ss->st, 1);
+      ++ss->pos;
+      if (ss->pos % ss->sb_max == 0) ss->solver.outer_update(ss->st);
+    }
+    if (times) {
+      times[0] = ss->log.t_inner - ti;
+      times[1] = ss->log.t_outer - to;
+    }
+    if (pcg_max)
+      for (size_t i = before; i < ss->log.pcg_iters.size(); ++i) pcg_max[i - before] = ss->log.pcg_iters[i];
+  });
+}
+
+void orc_session_destroy(orc_session* ss) { delete ss; }
 
 // PfeSolver::split_bregman on a caller-supplied state (solver.cpp:73-108);
 // state arrays are updated in place.  traj (max_iter*n*d, may be null)

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <limits>
 #include <map>
+#include <chrono>
 #include <random>
 #include <thread>
 #include <unordered_map>
@@ -29,6 +30,25 @@ void for_columns(long count, F&& body) {
     pool.emplace_back([&, w] {
       for (long j = w; j < count; j += t) body(j);
     });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Runs body(lo, hi) over [0, count) split into g_threads contiguous ranges.
+// Used only for per-element work whose results do not depend on the split
+// (k-means distances); every sum stays sequential.
+template <class F>
+void for_ranges(long count, F&& body) {
+  int t = static_cast<int>(std::min<long>(g_threads, count / 4096 + 1));
+  if (t <= 1) {
+    body(0L, count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const long chunk = (count + t - 1) / t;
+  for (int w = 0; w < t; ++w) {
+    const long lo = w * chunk, hi = std::min(count, lo + chunk);
+    if (lo < hi) pool.emplace_back([&, lo, hi] { body(lo, hi); });
   }
   for (auto& th : pool) th.join();
 }
@@ -470,11 +490,13 @@ double objective(const Csr& m, const Mat& y) {
 Mat shrink(const Mat& v, double gamma) {
   if (gamma < 0.0) throw ConfigError("shrink: gamma must be >= 0");
   Mat out(v.rows, v.cols);
-  for (size_t i = 0; i < v.a.size(); ++i) {
-    const double x = v.a[i];
-    const double mag = std::abs(x) - gamma;
-    out.a[i] = mag > 0.0 ? (x > 0.0 ? mag : -mag) : 0.0;
-  }
+  for_ranges(static_cast<long>(v.a.size()), [&](long lo, long hi) {
+    for (long i = lo; i < hi; ++i) {
+      const double x = v.a[i];
+      const double mag = std::abs(x) - gamma;
+      out.a[i] = mag > 0.0 ? (x > 0.0 ? mag : -mag) : 0.0;
+    }
+  });
   return out;
 }
 
@@ -621,10 +643,17 @@ void sb_loop(State& st, int max_iter, const IterCb& cb, const Csr& m, const Csr&
   for (long j = 0; j < d; ++j)
     for (long i = 0; i < n; ++i) rhs_quad(i, j) = hr * (sqrt_deg[i] * (st.p(i, j) - st.bregman(i, j)));
   for (int it = 0; it < max_iter; ++it) {
+    const auto t0 = std::chrono::steady_clock::now();
     Mat sb(ne, d);
-    for (size_t k = 0; k < sb.a.size(); ++k) sb.a[k] = st.split_s.a[k] - st.split_b.a[k];
+    // elementwise loops may run on several threads (no reductions: bitwise
+    // identical); every dot / norm stays sequential
+    for_ranges(static_cast<long>(sb.a.size()), [&](long lo, long hi) {
+      for (long k = lo; k < hi; ++k) sb.a[k] = st.split_s.a[k] - st.split_b.a[k];
+    });
     Mat rhs = spmm_dense(mt, sb);
-    for (size_t k = 0; k < rhs.a.size(); ++k) rhs.a[k] = hl * rhs.a[k] + rhs_quad.a[k];
+    for_ranges(static_cast<long>(rhs.a.size()), [&](long lo, long hi) {
+      for (long k = lo; k < hi; ++k) rhs.a[k] = hl * rhs.a[k] + rhs_quad.a[k];
+    });
     Mat y_old = st.y;
     Mat y_new;
     std::vector<PcgReport> reps = op.solve_multi(rhs, st.y, y_new);
@@ -646,9 +675,14 @@ void sb_loop(State& st, int max_iter, const IterCb& cb, const Csr& m, const Csr&
       throw NumericalError("split_bregman: NaN in embedding");
     Mat my = spmm_dense(m, st.y);
     Mat t(ne, d);
-    for (size_t k = 0; k < t.a.size(); ++k) t.a[k] = my.a[k] + st.split_b.a[k];
+    for_ranges(static_cast<long>(t.a.size()), [&](long lo, long hi) {
+      for (long k = lo; k < hi; ++k) t.a[k] = my.a[k] + st.split_b.a[k];
+    });
     st.split_s = shrink(t, 1.0 / lambda);
-    for (size_t k = 0; k < t.a.size(); ++k) st.split_b.a[k] += my.a[k] - st.split_s.a[k];
+    for_ranges(static_cast<long>(t.a.size()), [&](long lo, long hi) {
+      for (long k = lo; k < hi; ++k) st.split_b.a[k] += my.a[k] - st.split_s.a[k];
+    });
+    if (log) log->t_inner += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (cb) cb(it, st.y);
     const double den = mat_norm(y_old);
     if (conv_tol > 0.0 && den > 0.0) {
@@ -665,6 +699,21 @@ void PfeSolver::split_bregman(State& st, int max_iter, const IterCb& cb) const {
           true, log);
 }
 
+// solver.cpp:116-118: dy = sqrt(D) Y; P = project_orthogonal(dy + B); B += dy - P
+void PfeSolver::outer_update(State& st) const {
+  const auto t0 = std::chrono::steady_clock::now();
+  const long n = st.y.rows, d = st.y.cols;
+  Mat dy(n, d), a(n, d);
+  for (long j = 0; j < d; ++j)
+    for (long i = 0; i < n; ++i) {
+      dy(i, j) = sqrt_degree_[i] * st.y(i, j);
+      a(i, j) = dy(i, j) + st.bregman(i, j);
+    }
+  st.p = project_orthogonal(a);
+  for (size_t q = 0; q < dy.a.size(); ++q) st.bregman.a[q] += dy.a[q] - st.p.a[q];
+  if (log) log->t_outer += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // solver.cpp:110-126
 void PfeSolver::run_soc(State& st, int soc_max, int sb_max) const {
   for (int k = 0; k < soc_max; ++k) {
@@ -672,15 +721,8 @@ void PfeSolver::run_soc(State& st, int soc_max, int sb_max) const {
     std::fill(st.split_s.a.begin(), st.split_s.a.end(), 0.0);
     Mat y_old = st.y;
     split_bregman(st, sb_max);
+    outer_update(st);
     const long n = st.y.rows, d = st.y.cols;
-    Mat dy(n, d), a(n, d);
-    for (long j = 0; j < d; ++j)
-      for (long i = 0; i < n; ++i) {
-        dy(i, j) = sqrt_degree_[i] * st.y(i, j);
-        a(i, j) = dy(i, j) + st.bregman(i, j);
-      }
-    st.p = project_orthogonal(a);
-    for (size_t q = 0; q < dy.a.size(); ++q) st.bregman.a[q] += dy.a[q] - st.p.a[q];
     const double den = mat_norm(y_old);
     if (params_.conv_tol > 0.0 && den > 0.0) {
       Mat df(n, d);
@@ -930,7 +972,9 @@ Mat seed_centroids(const Mat& pts, int k, std::mt19937_64& rng) {
   const long f0 = first(rng);
   for (long t = 0; t < pts.cols; ++t) cen(0, t) = pts(f0, t);
   Vec d2(static_cast<size_t>(n));
-  for (long i = 0; i < n; ++i) d2[i] = row_dist2(pts, i, cen, 0);
+  for_ranges(n, [&](long lo, long hi) {
+    for (long i = lo; i < hi; ++i) d2[i] = row_dist2(pts, i, cen, 0);
+  });
   std::uniform_real_distribution<double> uni(0.0, 1.0);
   for (int c = 1; c < k; ++c) {
     double total = 0.0;
@@ -950,7 +994,9 @@ Mat seed_centroids(const Mat& pts, int k, std::mt19937_64& rng) {
       chosen = first(rng);
     }
     for (long t = 0; t < pts.cols; ++t) cen(c, t) = pts(chosen, t);
-    for (long i = 0; i < n; ++i) d2[i] = std::min(d2[i], row_dist2(pts, i, cen, c));
+    for_ranges(n, [&](long lo, long hi) {
+      for (long i = lo; i < hi; ++i) d2[i] = std::min(d2[i], row_dist2(pts, i, cen, c));
+    });
   }
   return cen;
 }
@@ -964,22 +1010,26 @@ std::vector<int> kmeans(const Mat& pts, int k, uint64_t seed, int max_iter) {
   std::mt19937_64 rng(seed);
   Mat cen = seed_centroids(pts, k, rng);
   std::vector<int> lab(static_cast<size_t>(n), 0);
+  Vec bdist(static_cast<size_t>(n));
   double prev = std::numeric_limits<double>::infinity();
   for (int iter = 0; iter < max_iter; ++iter) {
     double inertia = 0.0;
-    for (long i = 0; i < n; ++i) {
-      int best = 0;
-      double bd = row_dist2(pts, i, cen, 0);
-      for (int c = 1; c < k; ++c) {
-        const double dd = row_dist2(pts, i, cen, c);
-        if (dd < bd) {
-          bd = dd;
-          best = c;
+    for_ranges(n, [&](long lo, long hi) {
+      for (long i = lo; i < hi; ++i) {
+        int best = 0;
+        double bd = row_dist2(pts, i, cen, 0);
+        for (int c = 1; c < k; ++c) {
+          const double dd = row_dist2(pts, i, cen, c);
+          if (dd < bd) {
+            bd = dd;
+            best = c;
+          }
         }
+        lab[i] = best;
+        bdist[i] = bd;
       }
-      lab[i] = best;
-      inertia += bd;
-    }
+    });
+    for (long i = 0; i < n; ++i) inertia += bdist[i];  // point order, as cluster.cpp sums it
     Mat sums(k, pts.cols);
     std::vector<long> cnt(static_cast<size_t>(k), 0);
     for (long i = 0; i < n; ++i) {

@@ -151,6 +151,9 @@ Mat project_orthogonal(const Mat& a);                   // solver.cpp:27-41
 struct RunLog {
   std::vector<int> pcg_iters;  // per inner iteration, max over columns
   long inner_iterations = 0;
+  // wall seconds: solver construction + make_state, the inner split-Bregman
+  // iterations (rhs, PCG, shrink / Bregman update), the per-outer projection
+  double t_setup = 0.0, t_inner = 0.0, t_outer = 0.0;
 };
 
 class PfeSolver {  // solver.hpp:51-83, solver.cpp:43-136
@@ -159,6 +162,7 @@ class PfeSolver {  // solver.hpp:51-83, solver.cpp:43-136
   State make_state(const Mat& y0) const;
   void split_bregman(State& st, int max_iter, const IterCb& cb = {}) const;
   void run_soc(State& st, int soc_max, int sb_max) const;
+  void outer_update(State& st) const;  // solver.cpp:116-118 (the body of one outer iteration after the inner loop)
   State two_stage(const Mat& y0) const;
   const Csr& diff_matrix() const { return m_; }
   RunLog* log = nullptr;

@@ -90,5 +90,35 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     return LIB
 
 
+BINDING = PKG / "binding"
+REF_INCLUDE = Path("/root/reference/proj/core/include")
+EIGEN_STUB = PKG.parent / "tests" / "cpp" / "eigen_stub"
+REF_TEST = BINDING / "build" / "test_ref_binding"
+
+
+def build_ref_binding(verbose: bool = False) -> Path | None:
+    """Compiles the link-level backend (binding/pfe_core_b200.cpp) against the
+    reference's own headers into the test program tests/cpp/test_ref_binding.cpp
+    (with the test-only Eigen stub; Eigen3 is absent here).  Needs
+    /root/reference, so it runs in the build container only; the binary
+    travels with the repo snapshot to the GPU box like the library does."""
+    if not REF_INCLUDE.exists():
+        return None
+    src = [PKG.parent / "tests" / "cpp" / "test_ref_binding.cpp", BINDING / "pfe_core_b200.cpp"]
+    deps = src + [LIB, INCLUDE / "pfe_b200.h", EIGEN_STUB / "Eigen" / "Dense"]
+    if REF_TEST.exists() and REF_TEST.stat().st_mtime >= max(p.stat().st_mtime for p in deps):
+        return REF_TEST
+    REF_TEST.parent.mkdir(parents=True, exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", f"-I{EIGEN_STUB}", f"-I{REF_INCLUDE}", f"-I{INCLUDE}",
+           *map(str, src), f"-L{OUT_DIR}", "-lpfe_b200", "-Wl,-rpath,$ORIGIN/../../lib", "-o", str(REF_TEST)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return REF_TEST
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    print(build_ref_binding(verbose="-v" in sys.argv))

@@ -470,8 +470,8 @@ void team_gather_y(Team& t, double* out) {
     all.assign(slot * P, 0.0);
     for (size_t i = 0; i < t.size(); ++i) {
       const pfe_solver* S = t.S(i);
-      CK(cudaMemcpy(all.data() + i * slot, t.st[i]->y + S->own_vb * d, sizeof(double) * S->own_cnt * d,
-                    cudaMemcpyDeviceToHost));
+      stream_copy(all.data() + i * slot, t.st[i]->y + S->own_vb * d, sizeof(double) * S->own_cnt * d,
+                  cudaMemcpyDeviceToHost, S->stream);
     }
   } else {
     pfe_state* st = t.st[0];

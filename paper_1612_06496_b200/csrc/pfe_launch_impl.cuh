@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -27,19 +28,38 @@ inline void check_launch(const char* what) {
 }
 #define PFE_LAUNCHED(name) check_launch(name)
 
+// A value computed once per device (function attributes such as the
+// dynamic shared-memory opt-in are per device, and one process may drive
+// several devices from several host threads).
+struct PerDeviceValue {
+  std::mutex mu;
+  long v[64] = {};
+  bool set[64] = {};
+  template <class F>
+  long get(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!set[dev]) {
+      v[dev] = f();
+      set[dev] = true;
+    }
+    return v[dev];
+  }
+};
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
 // link-time dependency on libcuda).
 inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -103,13 +123,13 @@ struct Impl {
   template <int R, auto Kern>
   static int tiled_grid(size_t smem, const Grid<R>& g, int sm) {
     using G = TileGeo<R, D>;
-    static int per_sm = -1;  // one value per kernel instantiation
-    if (per_sm < 0) {
+    static PerDeviceValue cache;  // one value per kernel instantiation and device
+    const int per_sm = static_cast<int>(cache.get([&]() -> long {
       if (smem > 48 * 1024) cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int nb = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, Kern, G::NT, smem);
-      per_sm = nb < 1 ? 1 : nb;
-    }
+      return nb < 1 ? 1 : nb;
+    }));
     const long tiles = static_cast<long>((g.W + G::TW - 1) / G::TW) * ((g.H + G::TH - 1) / G::TH);
     return static_cast<int>(tiles < static_cast<long>(per_sm) * sm ? tiles : static_cast<long>(per_sm) * sm);
   }
@@ -226,16 +246,17 @@ struct Impl {
   template <int R>
   static ResPlan res_plan(const Grid<R>& g, int sms) {
     using G = ResGeo<D, R>;
-    static size_t avail = 0;
-    if (avail == 0) {
+    static PerDeviceValue cache;
+    const size_t avail = static_cast<size_t>(cache.get([]() -> long {
       int dev = 0, optin = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
       cudaFuncAttributes fa{};
       cudaFuncGetAttributes(&fa, k_sb_resident<D, R>);
-      avail = static_cast<size_t>(optin) - fa.sharedSizeBytes;
-      cudaFuncSetAttribute(k_sb_resident<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)avail);
-    }
+      const long av = static_cast<long>(optin) - static_cast<long>(fa.sharedSizeBytes);
+      cudaFuncSetAttribute(k_sb_resident<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)av);
+      return av;
+    }));
     ResPlan best;
     if (g.row_lo != 0 || g.row_hi != g.H) return best;  // single-domain solvers only
     const int max_blocks = std::min(sms, G::kMaxBlocks);
@@ -262,14 +283,14 @@ struct Impl {
   template <int R>
   static int persist_grid(const Grid<R>& g, const PersistIn& in, Launch l) {
     constexpr size_t smem = sizeof(double) * PersistGeo<D, R>::kSmem;
-    static int per_sm = -1;
-    if (per_sm < 0) {
+    static PerDeviceValue cache;
+    const int per_sm = static_cast<int>(cache.get([]() -> long {
       cudaFuncSetAttribute(k_sb_persistent<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int nb = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sb_persistent<D, R>, TileGeo<R, D>::NT, smem);
-      per_sm = nb;
-      if (per_sm < 1) throw std::runtime_error("persistent split-Bregman kernel does not fit on an SM");
-    }
+      return nb;
+    }));
+    if (per_sm < 1) throw std::runtime_error("persistent split-Bregman kernel does not fit on an SM");
     PersistArgs<R> a{};
     a.g = g;
     a.ybuf[0] = in.ybuf[0];

@@ -131,15 +131,15 @@ struct PinnedStage {
   char* buf[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
   static constexpr size_t kCap = 32u << 20;
-  bool ok = false, tried = false;
-  bool ready() {
-    if (!tried) {
-      tried = true;
+  bool ok = false;
+  std::once_flag once;
+  bool ready() {  // thread-safe lazy set-up (several solvers may share a device)
+    std::call_once(once, [this] {
       ok = cudaMallocHost(&buf[0], kCap) == cudaSuccess && cudaMallocHost(&buf[1], kCap) == cudaSuccess &&
            cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) == cudaSuccess;
       if (!ok) cudaGetLastError();
-    }
+    });
     return ok;
   }
 };
@@ -188,6 +188,8 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   const size_t nchunks = (bytes + cap - 1) / cap;
   auto issue = [&](size_t c) {
     const size_t off = c * cap, n = std::min(cap, bytes - off);
+    // an earlier copy_h2d (another solver's stream) may still be reading this buffer
+    CK(cudaStreamWaitEvent(s, ps.ev[c & 1], 0));
     CK(cudaMemcpyAsync(ps.buf[c & 1], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(ps.ev[c & 1], s));
   };
@@ -200,6 +202,26 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     if (c + 2 < nchunks) issue(c + 2);
   }
 }
+
+// Copy on a (non-blocking) solver stream and wait: ordered after that
+// stream's kernels, which a legacy-stream cudaMemcpy is not.
+void stream_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, bytes, kind, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+// Makes `dev` current for a scope and restores the caller's device after
+// (destroy entry points free memory and graphs that belong to `dev`).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 // Process-wide pool of pinned host control blocks: cudaMallocHost /
 // cudaFreeHost cost milliseconds each (cudaFreeHost synchronizes the
@@ -526,6 +548,7 @@ struct pfe_solver {
 
 struct pfe_state {
   pfe_solver* s = nullptr;
+  int device = -1;  // a state may outlive its solver; it frees on this device
   DevPool mem;
   double* ybuf[2] = {nullptr, nullptr};  // the two Y allocations (y / y2 alternate between them)
   double *y = nullptr, *y2 = nullptr, *p = nullptr, *breg = nullptr, *rq = nullptr, *r = nullptr;
@@ -1387,6 +1410,7 @@ void state_init_from_y0(pfe_state* st) {
 pfe_state* create_state(pfe_solver* S, const double* y0_host) {
   auto st = std::make_unique<pfe_state>();
   st->s = S;
+  st->device = S->device;
   st->mem.stream = S->stream;
   const size_t nd = static_cast<size_t>(S->n) * S->d;
   const size_t ed = static_cast<size_t>(S->edge_rows) * S->d;
@@ -1743,8 +1767,8 @@ void warn_from_log(pfe_solver* S, long lo, long hi) {
   const size_t k = static_cast<size_t>(hi - lo) * S->d;
   std::vector<int> stt(k);
   std::vector<double> rel(k);
-  CK(cudaMemcpy(stt.data(), S->log_st + lo * S->d, sizeof(int) * k, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(rel.data(), S->log_rel + lo * S->d, sizeof(double) * k, cudaMemcpyDeviceToHost));
+  stream_copy(stt.data(), S->log_st + lo * S->d, sizeof(int) * k, cudaMemcpyDeviceToHost, S->stream);
+  stream_copy(rel.data(), S->log_rel + lo * S->d, sizeof(double) * k, cudaMemcpyDeviceToHost, S->stream);
   for (size_t i = 0; i < k; ++i)
     if (stt[i] == pfe_dev::kMaxIter || stt[i] == pfe_dev::kFailed)
       std::fprintf(stderr, "pfe: inner solve column %d stopped at rel residual %g\n", static_cast<int>(i % S->d), rel[i]);
@@ -1878,7 +1902,11 @@ int pfe_solver_create(const pfe_graph* g, const pfe_params* p, const pfe_exec* x
   return guarded([&] { *out = create_solver(g, p, x); });
 }
 
-void pfe_solver_destroy(pfe_solver* s) { delete s; }
+void pfe_solver_destroy(pfe_solver* s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  delete s;
+}
 
 int pfe_solver_report(const pfe_solver* s, pfe_report* out) {
   return guarded([&] {
@@ -1893,8 +1921,8 @@ int pfe_solver_report(const pfe_solver* s, pfe_report* out) {
     const long cnt = std::min(s->inner_launched, s->log_cap);
     std::vector<int> it(static_cast<size_t>(cnt) * s->d), stt(static_cast<size_t>(cnt) * s->d);
     if (cnt > 0) {
-      CK(cudaMemcpy(it.data(), s->log_it, sizeof(int) * it.size(), cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(stt.data(), s->log_st, sizeof(int) * stt.size(), cudaMemcpyDeviceToHost));
+      stream_copy(it.data(), s->log_it, sizeof(int) * it.size(), cudaMemcpyDeviceToHost, s->stream);
+      stream_copy(stt.data(), s->log_st, sizeof(int) * stt.size(), cudaMemcpyDeviceToHost, s->stream);
     }
     r.inner_iterations = cnt;
     for (long i = 0; i < cnt; ++i) {
@@ -1918,9 +1946,9 @@ int64_t pfe_solver_pcg_log(const pfe_solver* s, int32_t* iters, int32_t* status,
     cnt = std::min<int64_t>(std::min(s->inner_launched, s->log_cap), cap);
     if (cnt <= 0) return;
     const size_t k = static_cast<size_t>(cnt) * s->d;
-    if (iters) CK(cudaMemcpy(iters, s->log_it, sizeof(int) * k, cudaMemcpyDeviceToHost));
-    if (status) CK(cudaMemcpy(status, s->log_st, sizeof(int) * k, cudaMemcpyDeviceToHost));
-    if (rel) CK(cudaMemcpy(rel, s->log_rel, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    if (iters) stream_copy(iters, s->log_it, sizeof(int) * k, cudaMemcpyDeviceToHost, s->stream);
+    if (status) stream_copy(status, s->log_st, sizeof(int) * k, cudaMemcpyDeviceToHost, s->stream);
+    if (rel) stream_copy(rel, s->log_rel, sizeof(double) * k, cudaMemcpyDeviceToHost, s->stream);
   });
   return rc == PFE_OK ? cnt : -rc;
 }
@@ -1947,7 +1975,7 @@ int64_t pfe_solver_trace(const pfe_solver* s, uint64_t* out, int64_t cap) {
   const int rc = guarded([&] {
     if (!s->trace) return;
     cnt = std::min<int64_t>(cap, kTraceCap);
-    CK(cudaMemcpy(out, s->trace, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost));
+    stream_copy(out, s->trace, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, s->stream);
   });
   return rc == PFE_OK ? cnt : -rc;
 }
@@ -1967,7 +1995,11 @@ int pfe_state_reset(pfe_state* st) {
   });
 }
 
-void pfe_state_destroy(pfe_state* st) { delete st; }
+void pfe_state_destroy(pfe_state* st) {
+  if (!st) return;
+  DeviceGuard g(st->device);
+  delete st;
+}
 
 int pfe_state_get(pfe_state* st, int32_t field, double* out) {
   return guarded([&] {
@@ -1993,7 +2025,7 @@ int pfe_state_get(pfe_state* st, int32_t field, double* out) {
     }
     const double* src = field == PFE_FIELD_SPLIT_B ? st->eb[st->eb_cur] : st->es;
     std::vector<double> rows(static_cast<size_t>(S->edge_rows) * d);
-    CK(cudaMemcpy(rows.data(), src, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost));
+    stream_copy(rows.data(), src, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost, S->stream);
     for (long e = 0; e < m; ++e)
       for (int j = 0; j < d; ++j) out[e + j * m] = rows[static_cast<size_t>(S->edge_row[e]) * d + j];
   });
@@ -2017,14 +2049,14 @@ int pfe_state_set(pfe_state* st, int32_t field, const double* in) {
     // materialize both edge arrays before a partial update of one of them
     std::vector<double> b_rows(static_cast<size_t>(S->edge_rows) * d, 0.0), s_rows(b_rows.size(), 0.0);
     if (!st->inner_zero) {
-      CK(cudaMemcpy(b_rows.data(), st->eb[st->eb_cur], sizeof(double) * b_rows.size(), cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(s_rows.data(), st->es, sizeof(double) * s_rows.size(), cudaMemcpyDeviceToHost));
+      stream_copy(b_rows.data(), st->eb[st->eb_cur], sizeof(double) * b_rows.size(), cudaMemcpyDeviceToHost, S->stream);
+      stream_copy(s_rows.data(), st->es, sizeof(double) * s_rows.size(), cudaMemcpyDeviceToHost, S->stream);
     }
     std::vector<double>& tgt = field == PFE_FIELD_SPLIT_B ? b_rows : s_rows;
     for (long e = 0; e < m; ++e)
       for (int j = 0; j < d; ++j) tgt[static_cast<size_t>(S->edge_row[e]) * d + j] = in[e + j * m];
-    CK(cudaMemcpy(st->eb[st->eb_cur], b_rows.data(), sizeof(double) * b_rows.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(st->es, s_rows.data(), sizeof(double) * s_rows.size(), cudaMemcpyHostToDevice));
+    stream_copy(st->eb[st->eb_cur], b_rows.data(), sizeof(double) * b_rows.size(), cudaMemcpyHostToDevice, S->stream);
+    stream_copy(st->es, s_rows.data(), sizeof(double) * s_rows.size(), cudaMemcpyHostToDevice, S->stream);
     st->inner_zero = false;
   });
 }
@@ -2217,6 +2249,15 @@ int pfe_pcg_solve_multi(int32_t n, const int32_t* row_ptr, const int32_t* col_id
       if (residual) residual[j] = col.rel;
       if (jacobi_fallback) jacobi_fallback[j] = S->jacobi_fallback ? 1 : 0;
     }
+  });
+}
+
+int pfe_ic0_probe(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, const double* values,
+                  int32_t* jacobi_fallback) {
+  return guarded([&] {
+    if (n < 0 || !row_ptr || !jacobi_fallback) config_error("pfe_ic0_probe: bad arguments");
+    pfe_host::IcFactorHost f;
+    *jacobi_fallback = pfe_host::ic0_factor(n, row_ptr, col_idx, values, f) ? 0 : 1;
   });
 }
 

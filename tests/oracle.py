@@ -111,6 +111,52 @@ def solve(g, p, y0, mode=0, full_state=False, log_cap=0):
     return res
 
 
+def solve_timed(g, p, y0, log_cap=100000):
+    """soc (mode 0) with the PCG log and wall seconds {setup, inner, outer}."""
+    n, d = g.n, p.dim
+    y0c = _cm(y0)
+    y = np.empty(n * d)
+    log = np.zeros(max(1, log_cap), np.int32)
+    ninner = C.c_long()
+    times = np.zeros(3)
+    pp = params(p)
+    _ck(lib().orc_solve_timed(0, *_g(g), dp(g.degree), C.byref(pp), dp(y0c), dp(y), None, None, None, None,
+                              ip(log), log_cap, C.byref(ninner), dp(times)))
+    return {"y": _un(y, n, d), "inner": ninner.value, "pcg_log": log[:min(log_cap, ninner.value)].copy(),
+            "t_setup": float(times[0]), "t_inner": float(times[1]), "t_outer": float(times[2])}
+
+
+class Session:
+    """A resident oracle solve (orc_session_*): built once, then stepped a few
+    inner iterations at a time along the soc schedule (bench.py CPU legs)."""
+
+    def __init__(self, g, p, y0):
+        self._h = C.c_void_p()
+        setup = C.c_double()
+        pp = params(p)
+        _ck(lib().orc_session_create(*_g(g), dp(g.degree), C.byref(pp), dp(_cm(y0)), C.byref(self._h),
+                                     C.byref(setup)))
+        self.setup_s = setup.value
+
+    def step(self, inner=1):
+        """-> (inner-iteration seconds, projection seconds, PCG iterations per inner iteration)."""
+        t = np.zeros(2)
+        k = np.zeros(max(1, inner), np.int32)
+        _ck(lib().orc_session_step(self._h, int(inner), dp(t), ip(k)))
+        return float(t[0]), float(t[1]), k[:inner].copy()
+
+    def close(self):
+        if self._h:
+            lib().orc_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def state_split_bregman(g, p, max_iter, y, pp_, breg, sb, ss, want_traj=False):
     n, d, m = g.n, p.dim, g.m
     arrs = [_cm(y).copy(order="F"), _cm(pp_).copy(order="F"), _cm(breg).copy(order="F"), _cm(sb).copy(order="F"),

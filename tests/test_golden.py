@@ -19,7 +19,7 @@ sys.path.insert(0, str(HERE / "golden"))
 
 import make_golden as MG  # noqa: E402
 
-FIXTURES = sorted((HERE / "golden").glob("*.npz"))
+FIXTURES = sorted(p for p in (HERE / "golden").glob("*.npz") if not p.name.startswith("full_"))
 IDS = [f.stem for f in FIXTURES]
 
 
