@@ -480,15 +480,18 @@ def run_gpu(args, rank, world, local):
     }
 
 
+_PINNED = []  # owners of the pinned host buffers handed out by pin()
+
+
 def pin(a):
     """A page-locked copy of a host array (torch pinned memory)."""
     import torch
 
     a = np.ascontiguousarray(a)
-    t = torch.empty(a.size * a.itemsize, dtype=torch.uint8, pin_memory=True)
-    out = t.numpy().view(a.dtype).reshape(a.shape)
+    t = torch.empty(max(1, a.size * a.itemsize), dtype=torch.uint8, pin_memory=True)
+    _PINNED.append(t)
+    out = t.numpy()[:a.size * a.itemsize].view(a.dtype).reshape(a.shape)
     out[...] = a
-    out._pin_owner = t  # noqa: keep the pinned buffer alive with the view
     return out
 
 

@@ -230,6 +230,12 @@ int pfe_band_plan(int32_t height, int32_t nranks, int32_t radius, int32_t rank, 
 int pfe_nccl_unique_id(uint8_t* out);
 int pfe_solver_create_band(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, const uint8_t* nccl_id,
                            int32_t nranks, int32_t rank, pfe_solver** out);
+/* Host only: the vertex-range partition pfe_solver_create_band builds for a
+ * general graph over `nranks` ranks (BFS storage order, contiguous ranges):
+ * per rank the owned vertices, the ghost rows it receives in every ghost
+ * exchange, and the owned rows it sends (one per peer that needs them).
+ * Arrays of nranks entries; any may be null. */
+int pfe_range_partition_stats(const pfe_graph* g, int32_t nranks, int64_t* owned, int64_t* ghosts, int64_t* sends);
 /* The same banded algorithm with `nbands` bands emulated in this process on
  * one device (device copies instead of NCCL): validates the decomposition.
  * mode 0: soc, 1: pfe_two_stage. */

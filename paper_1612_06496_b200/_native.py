@@ -82,6 +82,8 @@ _SIGS = {
                                                C.c_int32, C.POINTER(pfe_exec), _D, ITERATE_FN, C.c_void_p]),
     "pfe_pcg_solve_multi": (C.c_int, [C.c_int32, _I, _I, _D, C.c_int32, _D, _D, C.c_double, C.c_int32, C.c_int32,
                                       C.POINTER(pfe_exec), _D, _I, _I, _D, _I]),
+    "pfe_range_partition_stats": (C.c_int, [C.POINTER(pfe_graph), C.c_int32, C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "pfe_ic0_probe": (C.c_int, [C.c_int32, _I, _I, _D, _I]),
     "pfe_objective": (C.c_int, [C.POINTER(pfe_graph), C.c_int32, _D, C.POINTER(pfe_exec), _D]),
     "pfe_shrink": (C.c_int, [C.c_int64, _D, C.c_double, C.POINTER(pfe_exec), _D]),

@@ -542,6 +542,17 @@ def soc_banded(g: WeightedGraph, params: PfeParams, y0, nbands: int, two_stage: 
     return _from_colmajor(out, g.n, params.dim)
 
 
+def range_partition_stats(g: WeightedGraph, nranks: int) -> dict:
+    """Owned / ghost / sent rows per rank of the vertex-range partition a
+    BandSolver uses for a general graph (host only, no device)."""
+    own, gh, snd = (np.zeros(nranks, np.int64) for _ in range(3))
+    gc = g.to_c()
+    p64 = C.POINTER(C.c_int64)
+    _check(N.load().pfe_range_partition_stats(C.byref(gc), int(nranks), own.ctypes.data_as(p64),
+                                              gh.ctypes.data_as(p64), snd.ctypes.data_as(p64)))
+    return {"owned": own, "ghosts": gh, "sends": snd}
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(N.load().pfe_nccl_unique_id(buf))

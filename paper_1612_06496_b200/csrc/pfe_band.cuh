@@ -524,6 +524,48 @@ void band_timed(pfe_solver* S, F&& f) {
 // replica on both, updated identically (k_sb_pass writes the edges of ghost
 // owners too).  Rows of A and incidence lists keep the reference's term
 // order, so per-vertex arithmetic is that of the single-GPU solver.
+// Host-only statistics of the vertex-range partition create_range_solver
+// builds (same BFS storage order, same contiguous ranges): per rank the
+// owned vertices, the ghost rows it receives per exchange and the rows it
+// sends (with multiplicity per peer).
+void range_partition_stats(const pfe_graph* g, int nranks, int64_t* owned, int64_t* ghosts, int64_t* sends) {
+  if (!g || g->n < 1 || g->m < 0) config_error("vertex ranges: bad graph");
+  if (nranks < 1 || g->n < nranks) config_error("vertex ranges: bad rank count");
+  HostGraph hg{g->n, static_cast<long>(g->m), g->ei, g->ej, g->w, g->degree};
+  const int n = g->n, P = nranks;
+  const Incidence inc = build_incidence(hg);
+  const std::vector<int> pos = bfs_storage_order(n, inc.iptr, inc.inbr.data());
+  std::vector<int> vat(n);
+  for (int v = 0; v < n; ++v) vat[pos[v]] = v;
+  std::vector<int> start(P + 1);
+  for (int q = 0; q <= P; ++q) start[q] = static_cast<int>(static_cast<long>(n) * q / P);
+  for (int r = 0; r < P; ++r) {
+    const int s0 = start[r], s1 = start[r + 1];
+    std::vector<int> gh;
+    std::vector<std::vector<int>> sendl(P);
+    for (int l = 0; l < s1 - s0; ++l) {
+      const int v = vat[s0 + l];
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) {
+        const int pu = pos[inc.inbr[k]];
+        if (pu >= s0 && pu < s1) continue;
+        gh.push_back(pu);
+        const int q = static_cast<int>(std::upper_bound(start.begin(), start.end(), pu) - start.begin()) - 1;
+        sendl[q].push_back(l);
+      }
+    }
+    std::sort(gh.begin(), gh.end());
+    gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
+    long snd = 0;
+    for (auto& sl : sendl) {
+      std::sort(sl.begin(), sl.end());
+      snd += std::unique(sl.begin(), sl.end()) - sl.begin();
+    }
+    if (owned) owned[r] = s1 - s0;
+    if (ghosts) ghosts[r] = static_cast<int64_t>(gh.size());
+    if (sends) sends[r] = snd;
+  }
+}
+
 pfe_solver* create_range_solver(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int nranks, int rank,
                                 void* comm) {
   if (!g || !p) config_error("null graph or params");

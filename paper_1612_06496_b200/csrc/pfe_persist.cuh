@@ -611,10 +611,14 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
     }
     ebcur ^= 1;
     b_zero = false;
+    // NaN / Inf in this iteration's Y (solver.cpp:94): published before the
+    // barrier, so every block sees it after and the launch stops here, as the
+    // reference aborts the inner loop (the host then raises NumericalError)
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.ctl->nonfinite_y, 1);
     grid.sync();
     PFE_TRACE(8);
+    if (*reinterpret_cast<volatile int*>(&a.ctl->nonfinite_y)) break;
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.ctl->nonfinite_y, 1);
 }
 
 }  // namespace pfe_dev

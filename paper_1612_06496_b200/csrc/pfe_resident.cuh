@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(768, 1) k_sb_resident(PersistArgs<R> a) {
     }
     grid.sync();
     PFE_TRACE(1);
+    if (*reinterpret_cast<volatile int*>(&a.ctl->nonfinite_y)) break;  // NaN in the previous Y
     ring_load(a.r);
     reduce_partials_warp<3, D, NT>(part_i, nb, tot);
     ring_store(A2);
@@ -529,10 +530,12 @@ __global__ void __launch_bounds__(768, 1) k_sb_resident(PersistArgs<R> a) {
     }
     ebcur ^= 1;
     b_zero = false;
-    __syncthreads();
+    // NaN / Inf in this iteration's Y (solver.cpp:94): published now, seen by
+    // every block after the next grid barrier, where the launch stops
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.ctl->nonfinite_y, 1);
+    bad = 0;
     PFE_TRACE(8);
   }
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.ctl->nonfinite_y, 1);
 }
 
 }  // namespace pfe_dev

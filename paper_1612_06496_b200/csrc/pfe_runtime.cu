@@ -1453,6 +1453,8 @@ void check_flags(pfe_solver* S) {
   }
 }
 
+void warn_from_log(pfe_solver* S, long lo, long hi);
+
 PcgArgs pcg_args(pfe_state* st, const double* rhs) {
   pfe_solver* S = st->s;
   PcgArgs a{};
@@ -1658,6 +1660,7 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
     // Whole call in one cooperative launch; with a callback or the
     // relative-change test, one launch per inner iteration.
     const bool per_iter = mode.cb != nullptr || conv;
+    const long inner_before = S->inner_launched;
     for (int it = 0; it < max_iter;) {
       const int nrun = per_iter ? 1 : max_iter;
       pfe_host::PersistIn in{};
@@ -1702,6 +1705,9 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
       it += nrun;
       if (per_iter && after_iteration(it - 1)) break;
     }
+    // the reference's non-converged-column warnings (solver.cpp:87-92), from
+    // the device PCG log of this call's inner iterations
+    if (S->warn) warn_from_log(S, inner_before, S->inner_launched);
     return;
   }
   for (int it = 0; it < max_iter; ++it) {
@@ -2360,6 +2366,10 @@ int pfe_solver_create_band(const pfe_graph* g, const pfe_params* p, const pfe_ex
       throw;
     }
   });
+}
+
+int pfe_range_partition_stats(const pfe_graph* g, int32_t nranks, int64_t* owned, int64_t* ghosts, int64_t* sends) {
+  return guarded([&] { range_partition_stats(g, nranks, owned, ghosts, sends); });
 }
 
 int pfe_solve_banded(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t nbands, int32_t mode,

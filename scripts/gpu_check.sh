@@ -1,7 +1,17 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench_*.json
+#!/bin/bash
+# GPU check used during development: GPU tests, the default bench line and the
+# reference arm, with wall times.  Outputs under gpurun_out/.
+mkdir -p gpurun_out
+T0=$(date +%s)
+python -m pytest tests -m gpu -x -q -s -k "${PFE_TEST_K:-}" > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$? wall=$(( $(date +%s) - T0 ))s" >> gpurun_out/times.log
+if [ -n "${PFE_BENCH:-1}" ]; then
+  T0=$(date +%s)
+  python bench.py ${PFE_BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err
+  echo "bench rc=$? wall=$(( $(date +%s) - T0 ))s" >> gpurun_out/times.log
+fi
+if [ -n "${PFE_REF:-}" ]; then
+  T0=$(date +%s)
+  python bench.py --impl reference ${PFE_REF_ARGS:-} > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+  echo "reference rc=$? wall=$(( $(date +%s) - T0 ))s" >> gpurun_out/times.log
+fi
