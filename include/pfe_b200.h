@@ -242,6 +242,18 @@ int pfe_range_partition_stats(const pfe_graph* g, int32_t nranks, int64_t* owned
 int pfe_solve_banded(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t nbands, int32_t mode,
                      const double* y0, double* y_out, pfe_report* rep);
 
+/* Multi-GPU inside ONE call: soc (mode 0) or
+ * pfe_two_stage (mode 1) of one graph over the `ndev` distinct CUDA devices
+ * listed, from one host thread.  Pixel grids are cut into row bands, general
+ * graphs into vertex ranges (the same decomposition as
+ * pfe_solver_create_band); the communicators come from ncclCommInitAll and
+ * every NCCL call of a step is issued for all devices in one group.  The
+ * drop-in for pfe_two_stage(g, params, y0) (solver.cpp:191-193) on N GPUs.
+ * device_ms (may be null): device time of the solve, max over the GPUs. */
+int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t ndev,
+                        const int32_t* devices, int32_t mode, const double* y0, double* y_out, pfe_report* rep,
+                        double* device_ms);
+
 /* objective(M, Y) (solver.cpp:14-17) with M = difference_matrix(g). */
 int pfe_objective(const pfe_graph* g, int32_t d, const double* y, const pfe_exec* x, double* out);
 /* shrink(V, gamma) (solver.cpp:19-25), elementwise on count values. */

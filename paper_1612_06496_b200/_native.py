@@ -94,6 +94,8 @@ _SIGS = {
                                          C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.POINTER(_P)]),
     "pfe_solve_banded": (C.c_int, [C.POINTER(pfe_graph), C.POINTER(pfe_params), C.POINTER(pfe_exec), C.c_int32,
                                    C.c_int32, _D, _D, C.POINTER(pfe_report)]),
+    "pfe_solve_multi_gpu": (C.c_int, [C.POINTER(pfe_graph), C.POINTER(pfe_params), C.POINTER(pfe_exec), C.c_int32,
+                                      _I, C.c_int32, _D, _D, C.POINTER(pfe_report), _D]),
     "pfe_d_orthonormalize": (C.c_int, [C.c_int32, C.c_int32, _D, _D, _D]),
     "pfe_random_embedding": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _D, _D]),
     "pfe_kmeans": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_int32, C.c_uint64, C.c_int32, _I]),

@@ -542,6 +542,24 @@ def soc_banded(g: WeightedGraph, params: PfeParams, y0, nbands: int, two_stage: 
     return _from_colmajor(out, g.n, params.dim)
 
 
+def soc_multi_gpu(g: WeightedGraph, params: PfeParams, y0, devices, two_stage: bool = False,
+                  return_ms: bool = False):
+    """soc / pfe_two_stage of one graph over several GPUs from ONE call
+    (pfe_solve_multi_gpu): row bands (pixel grids) or vertex ranges (general
+    graphs), one band per listed device, NCCL communicators from
+    ncclCommInitAll.  With return_ms, also the device time (max over GPUs)."""
+    y0c = _colmajor(y0, g.n, params.dim)
+    out = np.empty(g.n * params.dim)
+    devs = np.ascontiguousarray(devices, np.int32)
+    gc, pc, xc = g.to_c(), params.to_c(), _exec(int(devs[0]), False, False, persistent=False)
+    rep = N.pfe_report()
+    ms = np.zeros(1)
+    _check(N.load().pfe_solve_multi_gpu(C.byref(gc), C.byref(pc), C.byref(xc), int(devs.size), N.iptr(devs),
+                                        1 if two_stage else 0, N.dptr(y0c), N.dptr(out), C.byref(rep), N.dptr(ms)))
+    y = _from_colmajor(out, g.n, params.dim)
+    return (y, float(ms[0])) if return_ms else y
+
+
 def range_partition_stats(g: WeightedGraph, nranks: int) -> dict:
     """Owned / ghost / sent rows per rank of the vertex-range partition a
     BandSolver uses for a general graph (host only, no device)."""

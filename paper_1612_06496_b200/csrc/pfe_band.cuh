@@ -38,6 +38,7 @@ struct NcclApi {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -60,6 +61,7 @@ NcclApi& nccl() {
   };
   api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
   api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
   api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
   api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
   api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
@@ -204,16 +206,40 @@ pfe_state* create_band_state(pfe_solver* S, const double* y0_global) {
 }
 
 // ------------------------------------------------------------------ team --
+// The bands a host thread drives: one band per process (NCCL, one GPU each),
+// every band of an image on its own GPU of this process (NCCL, one
+// communicator per device from ncclCommInitAll, pfe_solve_multi_gpu), or every
+// band emulated on one device (device copies, pfe_solve_banded).
 struct Team {
-  std::vector<pfe_state*> st;  // one band (NCCL) or every band (emulated)
+  std::vector<pfe_state*> st;
   bool emulated = false;
   pfe_solver* S(size_t i) const { return st[i]->s; }
   size_t size() const { return st.size(); }
 };
 
-void team_sync(Team& t) {
-  for (auto* st : t.st) CK(cudaStreamSynchronize(st->s->stream));
+// Makes member S's device current (kernel launches need their stream's
+// device); a no-op when the team lives on one device.
+inline pfe_solver* on(pfe_solver* S) {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != S->device) CK(cudaSetDevice(S->device));
+  return S;
 }
+
+void team_sync(Team& t) {
+  for (auto* st : t.st) CK(cudaStreamSynchronize(on(st->s)->stream));
+}
+
+// NCCL calls of every member of a multi-device team go into one group (one
+// host thread issues them for all communicators).
+struct NcclGroup {
+  const int unwinding = std::uncaught_exceptions();
+  NcclGroup() { nccl_check(nccl().GroupStart(), "ncclGroupStart"); }
+  ~NcclGroup() noexcept(false) {
+    const ncclResult_t r = nccl().GroupEnd();
+    if (std::uncaught_exceptions() == unwinding) nccl_check(r, "ncclGroupEnd");
+  }
+};
 
 // Emulated transport: a device copy ordered on the receiving band's stream
 // (the solver streams are non-blocking, so a legacy-stream copy would not be
@@ -229,7 +255,7 @@ void team_gather_totals(Team& t, int nq, bool spmv_partials, int nb_producer_of(
   const int d = t.S(0)->d, P = t.S(0)->nranks;
   const size_t cnt = static_cast<size_t>(nq) * d;
   for (auto* st : t.st) {
-    pfe_solver* S = st->s;
+    pfe_solver* S = on(st->s);
     S->tab->local_totals(nq, spmv_partials ? S->partials_b : S->partials, nb_producer_of(S, spmv_partials),
                          S->tot_local, S->stream);
   }
@@ -243,11 +269,14 @@ void team_gather_totals(Team& t, int nq, bool spmv_partials, int nb_producer_of(
     team_sync(t);
     return;
   }
-  pfe_solver* S = t.S(0);
   (void)P;
-  nccl_check(nccl().AllGather(S->tot_local, spmv_partials ? S->gathered_b : S->gathered_a, cnt, ncclDouble,
-                              static_cast<ncclComm_t>(S->comm), S->stream),
-             "ncclAllGather(totals)");
+  NcclGroup grp;
+  for (auto* st : t.st) {
+    pfe_solver* S = on(st->s);
+    nccl_check(nccl().AllGather(S->tot_local, spmv_partials ? S->gathered_b : S->gathered_a, cnt, ncclDouble,
+                                static_cast<ncclComm_t>(S->comm), S->stream),
+               "ncclAllGather(totals)");
+  }
 }
 
 // Refreshes the R halo rows of `field` (a [n_local][d] array) from the
@@ -274,19 +303,19 @@ void team_halo(Team& t, F&& field) {
     team_sync(t);
     return;
   }
-  pfe_state* st = t.st[0];
-  pfe_solver* S = st->s;
-  auto comm = static_cast<ncclComm_t>(S->comm);
-  nccl_check(nccl().GroupStart(), "ncclGroupStart");
-  if (S->rank > 0) {
-    nccl_check(nccl().Send(rows(st, S->row_lo), blk, ncclDouble, S->rank - 1, comm, S->stream), "ncclSend");
-    nccl_check(nccl().Recv(rows(st, 0), blk, ncclDouble, S->rank - 1, comm, S->stream), "ncclRecv");
+  NcclGroup grp;
+  for (pfe_state* st : t.st) {
+    pfe_solver* S = on(st->s);
+    auto comm = static_cast<ncclComm_t>(S->comm);
+    if (S->rank > 0) {
+      nccl_check(nccl().Send(rows(st, S->row_lo), blk, ncclDouble, S->rank - 1, comm, S->stream), "ncclSend");
+      nccl_check(nccl().Recv(rows(st, 0), blk, ncclDouble, S->rank - 1, comm, S->stream), "ncclRecv");
+    }
+    if (S->rank < S->nranks - 1) {
+      nccl_check(nccl().Send(rows(st, S->row_hi - R), blk, ncclDouble, S->rank + 1, comm, S->stream), "ncclSend");
+      nccl_check(nccl().Recv(rows(st, S->row_hi), blk, ncclDouble, S->rank + 1, comm, S->stream), "ncclRecv");
+    }
   }
-  if (S->rank < S->nranks - 1) {
-    nccl_check(nccl().Send(rows(st, S->row_hi - R), blk, ncclDouble, S->rank + 1, comm, S->stream), "ncclSend");
-    nccl_check(nccl().Recv(rows(st, S->row_hi), blk, ncclDouble, S->rank + 1, comm, S->stream), "ncclRecv");
-  }
-  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
 }
 
 int nb_producer(const pfe_solver* S, bool spmv) {
@@ -301,11 +330,22 @@ int nb_producer_init(const pfe_solver* S, bool) {
 }
 
 // One PCG solve of every band (pcg.cpp:40-114 for all d columns).
+//
+// The host does not read the device control block after every PCG
+// iteration.  It issues iterations in chunks and reads the control block
+// (one stream synchronisation) only at the end of a chunk: the first chunk
+// is as long as the previous solve (warm-started solves inside the
+// split-Bregman loop take about the same number of iterations), later ones
+// are short.  Iterations issued after every column stopped are no-ops: the
+// SpMV prologue finds no active column, clears any_active, and the update
+// and direction kernels return at once; their halo exchanges and gathers
+// move unchanged values.  So the chunking changes no result, and a typical
+// solve costs one host round trip instead of one per PCG iteration.
 void team_pcg(Team& t, const std::vector<const double*>& rhs) {
   const size_t B = t.size();
   std::vector<PcgArgs> a(B);
   for (size_t i = 0; i < B; ++i) {
-    pfe_solver* S = t.S(i);
+    pfe_solver* S = on(t.S(i));
     a[i] = pcg_args(t.st[i], rhs[i]);
     a[i].rd_a = S->gathered_a;
     a[i].rd_b = S->gathered_b;
@@ -314,46 +354,55 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
     a[i].nb_init = a[i].nb_update = a[i].nb_spmv = S->nranks;
   }
   const int maxit = t.S(0)->prm.pcg_max_iter;
-  for (size_t i = 0; i < B; ++i) t.S(i)->tab->pcg_init(t.S(i)->topo, a[i], t.S(i)->lv());
+  for (size_t i = 0; i < B; ++i) on(t.S(i))->tab->pcg_init(t.S(i)->topo, a[i], t.S(i)->lv());
   team_gather_totals(t, 3, false, nb_producer_init);
   team_halo(t, [](pfe_state* st) { return st->pb[0]; });
   auto spmv = [&](int k) {
     for (size_t i = 0; i < B; ++i) {
       a[i].phase = pfe_dev::pcg_phase(k);
-      t.S(i)->tab->pcg_spmv(t.S(i)->topo, a[i], t.S(i)->lv());
+      on(t.S(i))->tab->pcg_spmv(t.S(i)->topo, a[i], t.S(i)->lv());
     }
     team_gather_totals(t, 1, true, nb_producer);
   };
   const bool ranges = t.S(0)->part == 2;
-  int k = 1;
-  spmv(1);
-  for (;;) {
-    pfe_solver* S0 = t.S(0);
-    S0->read_ctl();  // every band took the same decision
-    if (!S0->h_ctl->any_active || k > maxit) break;
+  // one PCG iteration after the SpMV of iteration k: update k, SpMV k + 1
+  auto iteration = [&](int k) {
     if (k > 1 && !ranges) team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
     for (size_t i = 0; i < B; ++i) {
       a[i].phase = pfe_dev::pcg_phase(k);
-      t.S(i)->tab->pcg_update(t.S(i)->topo, a[i], t.S(i)->lv());
+      on(t.S(i))->tab->pcg_update(t.S(i)->topo, a[i], t.S(i)->lv());
     }
     team_gather_totals(t, 3, false, nb_producer);
-    ++k;
+    const int kn = k + 1;
     if (ranges) {
       // vertex ranges: p' = D^-1 r + beta p on owned rows, then its ghosts
       for (size_t i = 0; i < B; ++i) {
-        a[i].phase = pfe_dev::pcg_phase(k);
+        a[i].phase = pfe_dev::pcg_phase(kn);
         a[i].skip_pdir = 1;
-        t.S(i)->tab->pcg_pdir(t.S(i)->topo, a[i], t.S(i)->lv());
+        on(t.S(i))->tab->pcg_pdir(t.S(i)->topo, a[i], t.S(i)->lv());
       }
-      team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
+      team_halo(t, [kn](pfe_state* st) { return (kn & 1) ? st->pb[0] : st->pb[1]; });
     } else {
       team_halo(t, [](pfe_state* st) { return st->r; });
     }
-    spmv(k);
+    spmv(kn);
+  };
+  pfe_solver* S0 = t.S(0);
+  int k = 1;
+  spmv(1);
+  int chunk = std::max(1, S0->band_chunk_hint);
+  for (;;) {
+    for (int c = 0; c < chunk && k <= maxit; ++c) iteration(k++);
+    on(S0)->read_ctl();  // every band took the same decision
+    if (!S0->h_ctl->any_active || k > maxit) break;
+    chunk = 2;
   }
+  // the next solve's first chunk: this solve's iteration count
+  const int done = S0->h_ctl->iter;
+  for (size_t i = 0; i < B; ++i) t.S(i)->band_chunk_hint = std::max(1, done);
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
-    pfe_solver* S = st->s;
+    pfe_solver* S = on(st->s);
     const long vb = S->own_vb * S->d;
     const int cnt = S->own_cnt;
     S->tab->pcg_finalize(cnt, st->y + vb, st->y2 + vb, S->ctl, {S->grid_for(static_cast<long>(cnt) * S->d), S->stream, S->sm});
@@ -369,7 +418,7 @@ void team_split_bregman(Team& t, int max_iter) {
   std::vector<const double*> rhs(B);
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
-    pfe_solver* S = st->s;
+    pfe_solver* S = on(st->s);
     const long vb = S->own_vb;
     const int cnt = S->own_cnt;
     if (!st->rq_valid) {
@@ -388,7 +437,7 @@ void team_split_bregman(Team& t, int max_iter) {
     team_pcg(t, rhs);
     for (size_t i = 0; i < B; ++i) {
       pfe_state* st = t.st[i];
-      pfe_solver* S = st->s;
+      pfe_solver* S = on(st->s);
       SbArgs sa{};
       sa.y = st->y;
       sa.b_old = st->inner_zero ? nullptr : st->eb[st->eb_cur];
@@ -415,7 +464,7 @@ void team_project(Team& t) {
   const size_t fac = static_cast<size_t>(t.S(0)->qr_blocks) * d * d;
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
-    pfe_solver* S = st->s;
+    pfe_solver* S = on(st->s);
     const long vb = S->own_vb;
     const int cnt = S->own_cnt;
     S->tab->tsqr_local(cnt, st->y + vb * d, S->sqd + vb, st->breg + vb * d, S->rbuf, {S->qr_blocks, S->stream, S->sm});
@@ -427,13 +476,16 @@ void team_project(Team& t) {
         emu_copy(t.S(j), t.S(j)->rgather + i * fac, t.S(i)->rbuf, fac);
     team_sync(t);
   } else {
-    pfe_solver* S = t.S(0);
-    nccl_check(nccl().AllGather(S->rbuf, S->rgather, fac, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
-               "ncclAllGather(R factors)");
+    NcclGroup grp;
+    for (size_t i = 0; i < B; ++i) {
+      pfe_solver* S = on(t.S(i));
+      nccl_check(nccl().AllGather(S->rbuf, S->rgather, fac, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
+                 "ncclAllGather(R factors)");
+    }
   }
   for (size_t i = 0; i < B; ++i) {
     pfe_state* st = t.st[i];
-    pfe_solver* S = st->s;
+    pfe_solver* S = on(st->s);
     const long vb = S->own_vb;
     const int cnt = S->own_cnt;
     S->tab->tsqr_final(S->nranks * S->qr_blocks, S->rgather, S->wmat, S->ctl, {1, S->stream, S->sm});
@@ -444,7 +496,7 @@ void team_project(Team& t) {
 }
 
 void team_check(Team& t) {
-  for (auto* st : t.st) check_flags(st->s);
+  for (auto* st : t.st) check_flags(on(st->s));
 }
 
 // PfeSolver::run_soc (solver.cpp:110-126) over every band (fixed counts;
@@ -474,15 +526,21 @@ void team_gather_y(Team& t, double* out) {
                   cudaMemcpyDeviceToHost, S->stream);
     }
   } else {
-    pfe_state* st = t.st[0];
-    pfe_solver* S = st->s;
-    CK(cudaMemcpyAsync(S->ystage, st->y + S->own_vb * d, sizeof(double) * S->own_cnt * d, cudaMemcpyDeviceToDevice,
-                       S->stream));
-    nccl_check(nccl().AllGather(S->ystage, S->yall, slot, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
-               "ncclAllGather(Y)");
+    {
+      NcclGroup grp;
+      for (pfe_state* st : t.st) {
+        pfe_solver* S = on(st->s);
+        CK(cudaMemcpyAsync(S->ystage, st->y + S->own_vb * d, sizeof(double) * S->own_cnt * d,
+                           cudaMemcpyDeviceToDevice, S->stream));
+        nccl_check(nccl().AllGather(S->ystage, S->yall, slot, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
+                   "ncclAllGather(Y)");
+      }
+    }
+    pfe_solver* S = on(t.S(0));
     all.resize(slot * P);
     CK(cudaMemcpyAsync(all.data(), S->yall, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, S->stream));
     CK(cudaStreamSynchronize(S->stream));
+    for (size_t i = 1; i < t.size(); ++i) CK(cudaStreamSynchronize(on(t.S(i))->stream));
   }
   for (int p = 0; p < P; ++p) {
     long cnt, v0 = 0;
@@ -748,7 +806,7 @@ template <class F>
 void team_ghosts(Team& t, F&& field) {
   const int d = t.S(0)->d;
   for (auto* st : t.st) {
-    pfe_solver* S = st->s;
+    pfe_solver* S = on(st->s);
     for (const auto& pr : S->peers)
       S->tab->pack_rows(field(st), pr.send_rows, pr.send_cnt, S->sendbuf + pr.send_off * d, S->stream);
   }
@@ -769,19 +827,19 @@ void team_ghosts(Team& t, F&& field) {
     team_sync(t);
     return;
   }
-  pfe_state* st = t.st[0];
-  pfe_solver* S = st->s;
-  auto comm = static_cast<ncclComm_t>(S->comm);
-  nccl_check(nccl().GroupStart(), "ncclGroupStart");
-  for (const auto& pr : S->peers) {
-    if (pr.send_cnt > 0)
-      nccl_check(nccl().Send(S->sendbuf + pr.send_off * d, static_cast<size_t>(pr.send_cnt) * d, ncclDouble, pr.rank,
-                             comm, S->stream),
-                 "ncclSend");
-    if (pr.recv_cnt > 0)
-      nccl_check(nccl().Recv(field(st) + static_cast<size_t>(pr.recv_off) * d, static_cast<size_t>(pr.recv_cnt) * d,
-                             ncclDouble, pr.rank, comm, S->stream),
-                 "ncclRecv");
+  NcclGroup grp;
+  for (pfe_state* st : t.st) {
+    pfe_solver* S = on(st->s);
+    auto comm = static_cast<ncclComm_t>(S->comm);
+    for (const auto& pr : S->peers) {
+      if (pr.send_cnt > 0)
+        nccl_check(nccl().Send(S->sendbuf + pr.send_off * d, static_cast<size_t>(pr.send_cnt) * d, ncclDouble,
+                               pr.rank, comm, S->stream),
+                   "ncclSend");
+      if (pr.recv_cnt > 0)
+        nccl_check(nccl().Recv(field(st) + static_cast<size_t>(pr.recv_off) * d,
+                               static_cast<size_t>(pr.recv_cnt) * d, ncclDouble, pr.rank, comm, S->stream),
+                   "ncclRecv");
+    }
   }
-  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
 }

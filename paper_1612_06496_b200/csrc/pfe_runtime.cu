@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -420,7 +421,9 @@ struct pfe_solver {
   int nranks = 1, rank = 0;
   int band_h = 0, band_w = 0, band_rad = 0, band_r0 = 0, band_r1 = 0, band_lo = 0, band_maxrows = 0;
   long global_n = 0;
-  void* comm = nullptr;           // ncclComm_t when bands run in separate processes
+  void* comm = nullptr;           // ncclComm_t of this band (one per process, or one per device of a
+                                  // single-process multi-GPU team)
+  int band_chunk_hint = 4;        // PCG iterations the host issues before reading the control block
   double* tot_local = nullptr;    // [3 d] this band's totals
   double* gathered_a = nullptr;   // [ranks][3 d]
   double* gathered_b = nullptr;   // [ranks][d]
@@ -2395,6 +2398,76 @@ int pfe_solve_banded(const pfe_graph* g, const pfe_params* p, const pfe_exec* x,
     }
     team_gather_y(t, y_out);
     if (rep && pfe_solver_report(solvers[0].get(), rep) != PFE_OK) throw Error(PFE_CUDA_ERROR, g_last_error);
+  });
+}
+
+int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_t ndev,
+                        const int32_t* devices, int32_t mode, const double* y0, double* y_out, pfe_report* rep,
+                        double* device_ms) {
+  return guarded([&] {
+    if (!g || !p) config_error("null graph or params");
+    if (ndev < 1 || !devices) config_error("pfe_solve_multi_gpu: need at least one device");
+    std::vector<int> devs(devices, devices + ndev);
+    {
+      std::vector<int> u = devs;
+      std::sort(u.begin(), u.end());
+      if (std::adjacent_find(u.begin(), u.end()) != u.end())
+        config_error("pfe_solve_multi_gpu: devices must be distinct (pfe_solve_banded emulates bands on one device)");
+    }
+    for (int dv : devs) require_device(dv);
+    std::vector<ncclComm_t> comms(ndev, nullptr);
+    nccl_check(nccl().CommInitAll(comms.data(), ndev, devs.data()), "ncclCommInitAll");
+    const bool grid = g->grid_h > 0;
+    std::vector<pfe_solver*> solvers(ndev, nullptr);
+    std::vector<pfe_state*> states(ndev, nullptr);
+    auto cleanup = [&]() {
+      for (int b = 0; b < ndev; ++b) {
+        if (states[b]) {
+          cudaSetDevice(states[b]->device);
+          delete states[b];
+        }
+        if (solvers[b]) {
+          cudaSetDevice(solvers[b]->device);
+          delete solvers[b];  // destroys its communicator
+        } else if (comms[b]) {
+          nccl().CommDestroy(comms[b]);
+        }
+      }
+    };
+    try {
+      Team t;
+      for (int b = 0; b < ndev; ++b) {
+        pfe_exec xb = x ? *x : pfe_exec_default();
+        xb.device = devs[b];
+        solvers[b] = grid ? create_band_solver(g, p, &xb, ndev, b, comms[b])
+                          : create_range_solver(g, p, &xb, ndev, b, comms[b]);
+        states[b] = grid ? create_band_state(solvers[b], y0) : create_range_state(solvers[b], y0);
+        t.st.push_back(states[b]);
+      }
+      for (auto* S : solvers) CK(cudaEventRecord(on(S)->ev0, S->stream));
+      team_run_soc(t, p->soc_max, p->sb_max_stage1);
+      if (mode == 1 && p->sb_max_stage2 > 0) {
+        for (auto* S : solvers) S->ensure_log(p->sb_max_stage2);
+        team_split_bregman(t, p->sb_max_stage2);
+        team_check(t);
+      }
+      double worst = 0.0;
+      for (auto* S : solvers) {
+        CK(cudaEventRecord(on(S)->ev1, S->stream));
+        CK(cudaEventSynchronize(S->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+        worst = std::max(worst, static_cast<double>(ms));
+      }
+      for (auto* S : solvers) S->last_ms = worst;  // device time, max over the GPUs
+      if (device_ms) *device_ms = worst;
+      team_gather_y(t, y_out);
+      if (rep && pfe_solver_report(solvers[0], rep) != PFE_OK) throw Error(PFE_CUDA_ERROR, g_last_error);
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
   });
 }
 

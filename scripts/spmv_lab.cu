@@ -1,0 +1,251 @@
+// Kernel lab for the general-graph (k-NN, CSR) PCG SpMV q = A p, d = 16
+// (C5's operator).  NOT product code: variants of the gather loop timed side by
+// side on the real C5 matrix (scripts/spmv_lab.py builds it) to choose the
+// design that goes into csrc/.  Every variant sums each row left to right with
+// separate multiply and add (-fmad=false), so all must agree bit for bit.
+//
+// nvcc -O3 -gencode arch=compute_100a,code=sm_100a -fmad=false -lineinfo -shared -Xcompiler -fPIC \
+//      scripts/spmv_lab.cu -o scripts/libspmv_lab.so
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+namespace {
+
+constexpr int D = 16;
+
+// ---- V0: the shipped round-1 loop (8 lanes per row, 2 columns per lane,
+// batches of B gathers in registers, next batch's indices prefetched)
+template <int B, int MINB>
+__global__ void __launch_bounds__(256, MINB) v_regs(int n, const int* __restrict__ aptr, const int* __restrict__ acol,
+                                                   const double* __restrict__ aval, const double* __restrict__ p,
+                                                   double* __restrict__ q) {
+  const long total = static_cast<long>(n) * 8;
+  const long per = ((total + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x * blockDim.x;
+  const long e0 = static_cast<long>(blockIdx.x) * per + threadIdx.x;
+  long e1 = static_cast<long>(blockIdx.x + 1) * per;
+  e1 = e1 < total ? e1 : total;
+  for (long e = e0; e < e1; e += blockDim.x) {
+    const int v = static_cast<int>(e >> 3);
+    const int c0 = static_cast<int>(e & 7) * 2;
+    double q0 = 0.0, q1 = 0.0;
+    const int b = __ldg(aptr + v), en = __ldg(aptr + v + 1);
+    int cu[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) cu[j] = b + j < en ? __ldg(acol + b + j) : -1;
+    for (int k0 = b; k0 < en; k0 += B) {
+      double2 g[B];
+      double av[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) {
+          g[j] = __ldg(reinterpret_cast<const double2*>(p + static_cast<long>(cu[j]) * D + c0));
+          av[j] = __ldg(aval + k0 + j);
+        }
+      int cn[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) cn[j] = k0 + B + j < en ? __ldg(acol + k0 + B + j) : -1;
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        if (cu[j] >= 0) {
+          q0 += av[j] * g[j].x;
+          q1 += av[j] * g[j].y;
+        }
+#pragma unroll
+      for (int j = 0; j < B; ++j) cu[j] = cn[j];
+    }
+    reinterpret_cast<double2*>(q + static_cast<long>(v) * D + c0)[0] = make_double2(q0, q1);
+  }
+}
+
+// ---- V1: shared-memory gather ring.  A group of 8 lanes owns a contiguous
+// vertex range, i.e. a contiguous stream of nonzeros [k0, k1).  Step t
+// consumes nonzero t (landed in the ring L steps earlier) and issues the
+// cp.async gather of nonzero t + L (its column index was itself copied into
+// the index ring L steps earlier), so ~L row gathers per group are in flight
+// without holding registers.
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int L>
+struct RingGeo {
+  static constexpr int kGroups = 32;                              // 256 threads / 8 lanes
+  static constexpr int kGather = L * 8 * 16;                      // [L][8] double2
+  static constexpr int kVal = L * 8;                              // [L] double
+  static constexpr int kIdx = 2 * L * 4;                          // [2L] int
+  static constexpr int kPerGroup = kGather + kVal + kIdx;
+  static constexpr int kBytes = kGroups * kPerGroup;
+};
+
+template <int L, int MINB, bool kBalance>
+__global__ void __launch_bounds__(256, MINB) v_ring(int n, const int* __restrict__ aptr, const int* __restrict__ acol,
+                                                   const double* __restrict__ aval, const double* __restrict__ p,
+                                                   double* __restrict__ q) {
+  using G = RingGeo<L>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int grp = threadIdx.x >> 3, c = threadIdx.x & 7;
+  unsigned char* base = smem + grp * G::kPerGroup;
+  double2* gring = reinterpret_cast<double2*>(base);
+  double* vring = reinterpret_cast<double*>(base + G::kGather);
+  int* iring = reinterpret_cast<int*>(base + G::kGather + G::kVal);
+  // block range (equal vertex counts), then the group's share
+  const long vb0 = static_cast<long>(n) * blockIdx.x / gridDim.x, vb1 = static_cast<long>(n) * (blockIdx.x + 1) / gridDim.x;
+  int v0, v1;
+  if constexpr (kBalance) {
+    // split the block's nonzeros evenly among the groups (vertex-aligned)
+    const int kb0 = __ldg(aptr + vb0), kb1 = __ldg(aptr + vb1);
+    auto find = [&](long target) {  // first vertex v in [vb0, vb1] with aptr[v] >= target
+      long lo = vb0, hi = vb1;
+      while (lo < hi) {
+        const long mid = (lo + hi) >> 1;
+        if (__ldg(aptr + mid) >= target) hi = mid; else lo = mid + 1;
+      }
+      return static_cast<int>(lo);
+    };
+    v0 = find(kb0 + (static_cast<long>(kb1 - kb0) * grp) / G::kGroups);
+    v1 = find(kb0 + (static_cast<long>(kb1 - kb0) * (grp + 1)) / G::kGroups);
+  } else {
+    v0 = static_cast<int>(vb0 + (vb1 - vb0) * grp / G::kGroups);
+    v1 = static_cast<int>(vb0 + (vb1 - vb0) * (grp + 1) / G::kGroups);
+  }
+  const int k0 = __ldg(aptr + v0), k1 = __ldg(aptr + v1);
+  const int cnt = k1 - k0;
+  // warp-uniform step count
+  int steps = cnt;
+#pragma unroll
+  for (int o = 8; o < 32; o <<= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+  // prologue: indices of nonzeros [0, 2L), gathers of [0, L)
+  if (c == 0)
+    for (int t = 0; t < 2 * L; ++t)
+      if (t < cnt) cp_async4(iring + t, acol + k0 + t);
+  cp_commit();
+  cp_wait<0>();
+  __syncwarp();
+  for (int t = 0; t < L; ++t) {
+    if (t < cnt) {
+      const int u = iring[t];
+      cp_async16(gring + t * 8 + c, p + static_cast<long>(u) * D + 2 * c);
+      if (c == 0) cp_async8(vring + t, aval + k0 + t);
+    }
+    cp_commit();
+  }
+  int v = v0;
+  int kend = v < v1 ? __ldg(aptr + v + 1) - k0 : cnt;
+  int knext = v + 1 < v1 ? __ldg(aptr + v + 2) - k0 : cnt;
+  double q0 = 0.0, q1 = 0.0;
+  for (int t = 0; t < steps; ++t) {
+    cp_wait<L - 1>();
+    __syncwarp();
+    const int slot = t % L;
+    if (t < cnt) {
+      const double a = vring[slot];
+      const double2 g = gring[slot * 8 + c];
+      q0 += a * g.x;
+      q1 += a * g.y;
+      if (t + 1 == kend) {
+        reinterpret_cast<double2*>(q + static_cast<long>(v) * D + 2 * c)[0] = make_double2(q0, q1);
+        q0 = q1 = 0.0;
+        ++v;
+        // (no empty rows in A: the diagonal is always present)
+        kend = knext;
+        knext = v + 1 < v1 ? __ldg(aptr + v + 2) - k0 : cnt;
+      }
+    }
+    __syncwarp();
+    const int tn = t + L;
+    if (tn < cnt) {
+      const int u = iring[tn % (2 * L)];
+      cp_async16(gring + slot * 8 + c, p + static_cast<long>(u) * D + 2 * c);
+      if (c == 0) {
+        cp_async8(vring + slot, aval + k0 + tn);
+        if (tn + L < cnt) cp_async4(iring + (tn + L) % (2 * L), acol + k0 + tn + L);
+      }
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+}
+
+}  // namespace
+
+extern "C" {
+
+// variant ids: 0..3 registers (B, minBlocks) = (8,2) (8,3) (4,4) (12,2);
+// 10.. ring: L in {8, 16, 24, 32} x balance
+int lab_spmv(int variant, int n, const int* aptr, const int* acol, const double* aval, const double* p, double* q,
+             int reps, float* ms_out) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto launch = [&]() -> int {
+    int nb = 0;
+    switch (variant) {
+#define REGS(id, B, M)                                                              \
+  case id:                                                                          \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, v_regs<B, M>, 256, 0);       \
+    v_regs<B, M><<<sms * nb, 256>>>(n, aptr, acol, aval, p, q);                     \
+    return nb;
+      REGS(0, 8, 2)
+      REGS(1, 8, 3)
+      REGS(2, 4, 4)
+      REGS(3, 12, 2)
+      REGS(4, 16, 1)
+#define RING(id, L, M, BAL)                                                                                  \
+  case id: {                                                                                                 \
+    constexpr int sm = RingGeo<L>::kBytes;                                                                   \
+    cudaFuncSetAttribute(v_ring<L, M, BAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                 \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, v_ring<L, M, BAL>, 256, sm);                          \
+    if (nb < 1) return -1;                                                                                   \
+    v_ring<L, M, BAL><<<sms * nb, 256, sm>>>(n, aptr, acol, aval, p, q);                                     \
+    return nb;                                                                                               \
+  }
+      RING(10, 8, 4, false)
+      RING(11, 16, 2, false)
+      RING(12, 16, 3, false)
+      RING(13, 24, 2, false)
+      RING(14, 16, 2, true)
+      RING(15, 24, 2, true)
+      RING(16, 12, 3, true)
+      RING(17, 32, 1, true)
+      default:
+        return -2;
+    }
+  };
+  int nb = launch();
+  if (nb < 0) return nb;
+  cudaDeviceSynchronize();
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_out = ms / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    std::fprintf(stderr, "lab_spmv variant %d: %s\n", variant, cudaGetErrorString(err));
+    return -3;
+  }
+  return nb;
+}
+}

@@ -106,3 +106,40 @@ def test_vertex_ranges_two_stage_disconnected_and_repeatable():
     r2 = api.soc_banded(g, prm, y0, 3, two_stage=True)
     assert np.array_equal(r1, r2)
     assert rel(r1, api.pfe_two_stage(g, prm, y0)) <= 1e-11
+
+
+# ------------------------------------------- multi-GPU inside one call ------
+def gpu_count():
+    import torch
+
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("kind", ["grid8", "grid24", "knn"])
+def test_multi_gpu_one_call_matches_single_gpu(kind):
+    """pfe_solve_multi_gpu (ncclCommInitAll, one band per listed device, the
+    NCCL transport) over every visible GPU (one on the test box: a one-rank
+    communicator, halos absent, totals and R factors all-gathered through
+    NCCL) gives the single-GPU solver's answer."""
+    if kind == "knn":
+        g = knn_points_graph(900, 8, 5)
+    else:
+        g = image_graph(41, 50, 4, 1 if kind == "grid8" else 2)
+    d = 4
+    prm = params(d, soc=2, sb=4, stage2=3)
+    y0 = api.random_embedding(g.n, d, 2, g.degree)
+    devs = list(range(gpu_count()))
+    y, ms = api.soc_multi_gpu(g, prm, y0, devs, two_stage=True, return_ms=True)
+    ref = api.pfe_two_stage(g, prm, y0, persistent=False)
+    err = rel(y, ref)
+    print(f"{kind}: {len(devs)} GPU(s) rel err {err:.3e}, {ms:.2f} ms")
+    assert err <= 1e-11
+    assert ms > 0.0
+
+
+def test_multi_gpu_rejects_repeated_devices():
+    g = image_graph(20, 20, 1, 1)
+    prm = params(2)
+    y0 = api.random_embedding(g.n, 2, 1, g.degree)
+    with pytest.raises(api.ConfigError, match="distinct"):
+        api.soc_multi_gpu(g, prm, y0, [0, 0])
