@@ -299,6 +299,20 @@ int pfe_gmm_init_device(int32_t n, const double* features, int32_t k, uint64_t s
 int pfe_knn_graph(int32_t n, int32_t dim, const double* points, int32_t k, int32_t device, int32_t* ei, int32_t* ej,
                   double* w, double* degree, int64_t* m_out, double* sigma_out);
 
+/* Pixel-grid graph builder on the GPU (configs C2-C4):
+ * build_image_graph (graph.cpp:105-159) generalised to the 8-neighbour
+ * (radius 1) and 5x5 (radius 2) neighbourhoods, as the harness builder
+ * paper_1612_06496_b200/inputs.py grid_graph defines it: heat kernel
+ * w = exp(-|drgb|^2 / (2 sigma_rgb^2) [- |dxy|^2 / (2 sigma_xy^2) if sigma_xy > 0]),
+ * weights below 1e-12 dropped, an isolated pixel keeps its strongest
+ * incident candidate floored at 1e-12, edges lexicographic (i < j), degree
+ * summed in edge order (graph.cpp:15-22).  rgb: row-major height x width x 3.
+ * ei / ej / w need capacity n * (4 or 12), degree n; *m_out = edge count.
+ * Weights equal the host builder's up to the last ulp of exp. */
+int pfe_grid_graph(int32_t height, int32_t width, const double* rgb, double sigma_rgb, int32_t radius,
+                   double sigma_xy, int32_t device, int32_t* ei, int32_t* ej, double* w, double* degree,
+                   int64_t* m_out);
+
 #ifdef __cplusplus
 }
 #endif

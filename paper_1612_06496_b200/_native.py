@@ -103,6 +103,8 @@ _SIGS = {
     "pfe_gmm_init_device": (C.c_int, [C.c_int32, _D, C.c_int32, C.c_uint64, _D, C.c_int32, _D, _D, _D, _D]),
     "pfe_knn_graph": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_int32, C.c_int32, _I, _I, _D, _D,
                                 C.POINTER(C.c_int64), _D]),
+    "pfe_grid_graph": (C.c_int, [C.c_int32, C.c_int32, _D, C.c_double, C.c_int32, C.c_double, C.c_int32, _I, _I,
+                                 _D, _D, C.POINTER(C.c_int64)]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

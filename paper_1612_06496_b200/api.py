@@ -503,6 +503,26 @@ def gmm_init_embedding(features, k: int, seed: int, degree, device: int = 0, mod
     return y0
 
 
+def grid_graph_gpu(rgb, sigma_rgb: float, radius: int = 1, sigma_xy: Optional[float] = None,
+                   device: int = 0) -> "WeightedGraph":
+    """Heat-kernel pixel-grid graph built on the GPU (pfe_grid_graph); same
+    definition as inputs.grid_graph (the host builder, graph.cpp:105-159
+    semantics), with the grid hint set."""
+    img = np.ascontiguousarray(rgb, dtype=np.float64)
+    h, wd, _ = img.shape
+    n = h * wd
+    cap = n * (4 if radius == 1 else 12)
+    ei, ej = np.empty(cap, np.int32), np.empty(cap, np.int32)
+    w, deg = np.empty(cap), np.empty(n)
+    m = C.c_int64()
+    _check(N.load().pfe_grid_graph(h, wd, N.dptr(img), float(sigma_rgb), int(radius),
+                                   float(sigma_xy) if sigma_xy is not None else 0.0, int(device), N.iptr(ei),
+                                   N.iptr(ej), N.dptr(w), N.dptr(deg), C.byref(m)))
+    mm = m.value
+    return WeightedGraph(n, ei[:mm].copy(), ej[:mm].copy(), w[:mm].copy(), deg, float(sigma_rgb),
+                         grid=(h, wd, int(radius)))
+
+
 def knn_graph_gpu(points, k: int, device: int = 0) -> "WeightedGraph":
     """Union-symmetrised k-NN heat-kernel graph built on the GPU (pfe_knn_graph);
     same definition as inputs.knn_graph (the host builder)."""

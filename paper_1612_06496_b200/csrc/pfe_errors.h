@@ -31,6 +31,8 @@ struct IcFactorHost {
 bool ic0_factor(int n, const int* ptr, const int* idx, const double* val, IcFactorHost& out);
 void gmm_init_device(int n, const double* feat, int k, uint64_t seed, const double* degree, double* y_out,
                      double* means_out, double* vars_out, double* weights_out);
+long grid_graph_device(int H, int W, const double* rgb, double sigma_rgb, int radius, double sigma_xy, int32_t* ei,
+                       int32_t* ej, double* w, double* degree);
 long knn_graph_from_lists(int n, int k, const double* d2, const int32_t* idx, int32_t* ei, int32_t* ej, double* w,
                           double* degree, double* sigma_out);
 

@@ -2536,6 +2536,16 @@ int pfe_knn_graph(int32_t n, int32_t dim, const double* points, int32_t k, int32
   });
 }
 
+int pfe_grid_graph(int32_t height, int32_t width, const double* rgb, double sigma_rgb, int32_t radius,
+                   double sigma_xy, int32_t device, int32_t* ei, int32_t* ej, double* w, double* degree,
+                   int64_t* m_out) {
+  return guarded([&] {
+    if (!rgb || !ei || !ej || !w || !degree || !m_out) config_error("grid_graph: null argument");
+    require_device(device);
+    *m_out = pfe_host::grid_graph_device(height, width, rgb, sigma_rgb, radius, sigma_xy, ei, ej, w, degree);
+  });
+}
+
 }  // extern "C"
 
 namespace pfe_host {

@@ -151,6 +151,7 @@ class Config:
     y0_seed: int
     truth: Optional[np.ndarray] = None
     description: str = ""
+    image: Optional[np.ndarray] = None  # (H, W, 3) RGB of the image configs
 
 
 def _params(d, soc, sb, tol):
@@ -191,19 +192,19 @@ def make_config(name: str, seed: int = 0, scale: Optional[Tuple[int, int]] = Non
         img, lab = voronoi_image(h, w, 8, 0.05, rng)
         g = grid_graph(img, 0.1, 1)
         return Config("c2", g, _params(4, 10, 20, 1e-6), 8, seed, lab.ravel(),
-                      f"{w}x{h} Voronoi RGB (8 regions, noise 0.05), 8-nbr grid, d=4, 10x20")
+                      f"{w}x{h} Voronoi RGB (8 regions, noise 0.05), 8-nbr grid, d=4, 10x20", img)
     if name == "c3":
         h, w = scale or (1024, 1024)
         img, lab = voronoi_image(h, w, 32, 0.03, rng, gradient=1.0 / 512.0)
         g = grid_graph(img, 0.1, 2, sigma_xy=2.0)
         return Config("c3", g, _params(8, 10, 30, 1e-7), 32, seed, lab.ravel(),
-                      f"{w}x{h} Voronoi RGB with gradients (32 regions), 5x5 grid RGB+xy, d=8, 10x30")
+                      f"{w}x{h} Voronoi RGB with gradients (32 regions), 5x5 grid RGB+xy, d=8, 10x30", img)
     if name == "c4":
         h, w = scale or (4096, 4096)
         img, lab = voronoi_image(h, w, 256, 0.05, rng)
         g = grid_graph(img, 0.1, 1)
         return Config("c4", g, _params(8, 5, 20, 1e-6), 256, seed, lab.ravel(),
-                      f"{w}x{h} Voronoi RGB (256 regions), 8-nbr grid, d=8, 5x20")
+                      f"{w}x{h} Voronoi RGB (256 regions), 8-nbr grid, d=8, 5x20", img)
     if name == "c5":
         n = scale[0] if scale else 1_000_000
         means = rng.uniform(-10.0, 10.0, size=(32, 16))
