@@ -57,13 +57,20 @@ struct Ctl {
 
 // --------------------------------------------------------------------------
 // Column grouping: each thread owns V consecutive columns of one vertex row;
-// TPV = D / V threads cooperate on a row.  Even D that divide 32-lane warps
-// use 16-byte double2 accesses; other D use one thread per row.
+// TPV = D / V threads cooperate on a row.  d = 16 rows (128 B) are read as
+// four 32-byte (256-bit, LDG.256) pieces: a warp instruction then gathers 8
+// rows instead of 4, which halves the load instructions of the
+// gather-bound general-graph kernels (C5; SpMV 495 -> 428 us in
+// scripts/spmv_lab.py).  Other even D that divide 32-lane warps use 16-byte
+// double2 accesses; the rest use one thread per row.
 template <int D>
 struct Cols {
-  static constexpr int V = (D == 2 || D == 4 || D == 8 || D == 16) ? 2 : D;
+  static constexpr int V = D == 16 ? 4 : ((D == 2 || D == 4 || D == 8) ? 2 : D);
   static constexpr int TPV = D / V;
 };
+// row gathers issued together per batch by the general-graph kernels
+template <int V>
+constexpr int kGatherBatch = V >= 4 ? 4 : 8;
 
 template <int V>
 struct Row {
@@ -73,7 +80,13 @@ struct Row {
 template <int V>
 __device__ __forceinline__ Row<V> ldg_row(const double* __restrict__ p) {
   Row<V> r;
-  if constexpr (V % 2 == 0) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < V / 4; ++k)
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(r.a[4 * k]), "=d"(r.a[4 * k + 1]), "=d"(r.a[4 * k + 2]), "=d"(r.a[4 * k + 3])
+                   : "l"(p + 4 * k));
+  } else if constexpr (V % 2 == 0) {
 #pragma unroll
     for (int k = 0; k < V / 2; ++k) {
       const double2 t = __ldg(reinterpret_cast<const double2*>(p) + k);
@@ -92,7 +105,14 @@ __device__ __forceinline__ Row<V> ldg_row(const double* __restrict__ p) {
 template <int V>
 __device__ __forceinline__ Row<V> ld_row(const double* p) {
   Row<V> r;
-  if constexpr (V % 2 == 0) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < V / 4; ++k)
+      asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(r.a[4 * k]), "=d"(r.a[4 * k + 1]), "=d"(r.a[4 * k + 2]), "=d"(r.a[4 * k + 3])
+                   : "l"(p + 4 * k)
+                   : "memory");
+  } else if constexpr (V % 2 == 0) {
 #pragma unroll
     for (int k = 0; k < V / 2; ++k) {
       const double2 t = reinterpret_cast<const double2*>(p)[k];
@@ -108,7 +128,13 @@ __device__ __forceinline__ Row<V> ld_row(const double* p) {
 
 template <int V>
 __device__ __forceinline__ void st_row(double* p, const Row<V>& r) {
-  if constexpr (V % 2 == 0) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < V / 4; ++k)
+      asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4 * k), "d"(r.a[4 * k]), "d"(r.a[4 * k + 1]),
+                   "d"(r.a[4 * k + 2]), "d"(r.a[4 * k + 3])
+                   : "memory");
+  } else if constexpr (V % 2 == 0) {
 #pragma unroll
     for (int k = 0; k < V / 2; ++k) reinterpret_cast<double2*>(p)[k] = make_double2(r.a[2 * k], r.a[2 * k + 1]);
   } else {

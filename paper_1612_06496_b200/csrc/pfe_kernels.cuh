@@ -248,14 +248,17 @@ __device__ __forceinline__ bool update_prologue(const PcgArgs& a, ColView<D>& cv
   return true;  // even with every column failed, write (inert) partials
 }
 
-// Vertex rows of a gather-bound kernel.  kContig (general graphs): each
-// block takes one contiguous range of (vertex, column group) items, so the
-// successive chunks a block (and its SM) processes are neighbours in the
-// locality storage order and share gathered rows in L1 (SpMV-type kernels).
-// Otherwise grid-stride order: the whole GPU sweeps one window of the
-// storage order, so an edge row read by both endpoints is still in L2 for
-// the second read (split-Bregman pass).
-template <int TPV, bool kContig = true, class Topo>
+// Vertex rows of a gather-bound kernel: grid-stride order, so block b takes
+// chunks b, b + nb, ... of blockDim / TPV consecutive vertices and the whole
+// GPU sweeps one window of the storage order at a time.  For general graphs
+// in breadth-first storage order the rows gathered at any moment then come
+// from a window a few MB wide that stays in L2 (C5 SpMV: DRAM reads 1.34 GB
+// -> 0.45 GB = compulsory, 429 -> 319 us, scripts/spmv_lab.py), and an edge
+// row read by both endpoints is often still in L2 for the second read
+// (split-Bregman pass).  kContig (one contiguous range per block; more L1
+// reuse, but the whole vector is gathered at once and misses L2) is kept
+// for comparison.
+template <int TPV, bool kContig = false, class Topo>
 __device__ __forceinline__ void row_range(const Topo& topo, long& e0, long& e1, long& step) {
   const long first = static_cast<long>(topo.vbeg()) * TPV, total = static_cast<long>(topo.vend()) * TPV;
   if constexpr (Topo::kGrid || !kContig) {
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_init(Topo topo, PcgArgs a) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
     double ax[V] = {};
-    topo.template visitA_b<8>(
+    topo.template visitA_b<kGatherBatch<V>>(
         v, [&](int u) { return ldg_row<V>(a.x0 + static_cast<long>(u) * D + c0); },
         [&](double av, const Row<V>& xu) {
 #pragma unroll
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_spmv(Topo topo, PcgArgs a) {
       // CSR rows: p' was formed for every vertex by k_pcg_pdir (one gather per
       // neighbour instead of three); first iteration: p = z from the init
       pv = ldg_row<V>(pnew + static_cast<long>(v) * D + c0);
-      topo.template visitA_b<8>(
+      topo.template visitA_b<kGatherBatch<V>>(
           v, [&](int u) { return ldg_row<V>(pnew + static_cast<long>(u) * D + c0); },
           [&](double av, const Row<V>& pu) {
 #pragma unroll
@@ -549,13 +552,13 @@ struct SbArgs {
 // right-hand side (solver.cpp:83-84) is accumulated from the same edge values:
 // rhs_v = hl * sum_e M_ev (s_e - b_e') + rq_v.
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock, 3) k_sb_pass(Topo topo, SbArgs a) {
+__global__ void __launch_bounds__(kBlock, D == 16 ? 2 : 3) k_sb_pass(Topo topo, SbArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   const long total = static_cast<long>(topo.vend()) * TPV;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   int bad = 0;
   long e0, e1, step;
-  row_range<TPV, false>(topo, e0, e1, step);
+  row_range<TPV>(topo, e0, e1, step);
   for (long e = e0; e < e1; e += step) {
     const int v = static_cast<int>(e / TPV);
     const int c0 = static_cast<int>(e - static_cast<long>(v) * TPV) * V;
@@ -577,7 +580,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sb_pass(Topo topo, SbArgs a) {
       }
       return g;
     };
-    topo.template visitE_b<4>(v, load, [&](int u, double w, long slot, bool fwd, const YB& g) {
+    topo.template visitE_b<(V >= 4 ? 3 : 4)>(v, load, [&](int u, double w, long slot, bool fwd, const YB& g) {
       const Row<V>& yu = g.y;
       const Row<V>& bo = g.b;
       Row<V> bn, sv;

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
     k_sb_persistent(const __grid_constant__ PersistArgs<R> a) {
   using G = TileGeo<R, D>;
   using T = GridTopo<R>;
-  constexpr int V = G::V;
+  constexpr int V = PairMode<R, D>::V;
   constexpr int NT = G::NT;
   extern __shared__ __align__(1024) double smem[];  // 1024: TMA box destinations
   __shared__ PersistCols<D> pc;
@@ -219,17 +219,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
         const double* Dg = P + G::kI_Dg;
         const double* Iv = P + G::kI_Iv;
         const TileIdx ti = tile_of<R, D>(g, t);
-        for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-          const double ax = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
-          const double b = Bv[tv * D + c];
-          const double rr = b - ax;
-          const double z = Iv[tv] * rr;
-          a.r[v * D + c] = rr;
-          a.pbuf[0][v * D + c] = z;
-          acc[0][k] += b * b;
-          acc[1][k] += rr * rr;
-          acc[2][k] += rr * z;
-        });
+        tile_init_body<R, D, V>(g, ti, P, Wt, Bv, Dg, Iv, a.r, a.pbuf[0], acc);
         if (bulk) fence_proxy_async();  // zero-fill stores before later async writes
         __syncthreads();
         buf ^= 1;
@@ -354,13 +344,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
             __syncthreads();
           }
           const TileIdx ti = tile_of<R, D>(g, t);
-          for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-            const double qv = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
-            const double pv = P[hpos * D + c];
-            a.q[v * D + c] = qv;
-            if (!first) pnew[v * D + c] = pv;
-            acc[0][k] += pv * qv;
-          });
+          tile_spmv_body<R, D, V>(g, ti, P, Wt, Dg, a.q, first ? nullptr : pnew, acc);
           // p' was formed in place (generic proxy); a later TMA copy into
           // this buffer (async proxy) must be ordered after those writes
           if (tma || bulk) fence_proxy_async();

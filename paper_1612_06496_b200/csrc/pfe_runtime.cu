@@ -507,7 +507,7 @@ struct pfe_solver {
   int grid_for(long threads) const {
     return static_cast<int>(std::max<long>(1, std::min<long>((threads + pfe_dev::kBlock - 1) / pfe_dev::kBlock, max_grid)));
   }
-  int tpv() const { return (d == 2 || d == 4 || d == 8 || d == 16) ? d / 2 : 1; }
+  int tpv() const { return d == 16 ? 4 : ((d == 2 || d == 4 || d == 8) ? d / 2 : 1); }  // pfe_dev::Cols<d>::TPV
   pfe_host::Launch lv() const { return {grid_for(static_cast<long>(n) * tpv()), stream, sm}; }  // vertex kernels
   pfe_host::Launch le() const { return {grid_for(static_cast<long>(n) * d), stream, sm}; }     // elementwise
   pfe_host::Launch lr() const { return {grid_for(n), stream, sm}; }                            // row kernels

@@ -248,11 +248,160 @@ __device__ __forceinline__ double tile_apply_A(const double* P, const double* Ct
   return q;
 }
 
+// Pair mode (even D, NV * D == 4 * NT): a thread evaluates two vertically
+// adjacent pixels (tile rows 2i and 2i + 1) for two adjacent columns.  The
+// terms of a row of A, in the order tile_apply_A adds them (backward slots
+// S-1..0, the diagonal, forward slots 0..S-1), are exactly the positions of
+// the (2R+1) x (2R+1) window around the pixel in raster order.  The pair
+// therefore walks the (2R+2) x (2R+1) window covering both pixels row by
+// row: every P position is read once (16 bytes: both columns) and used by
+// both pixels, each pixel still adding its terms in its own raster order.
+// Same products, same selected additions in the same sequence as
+// tile_apply_A -- bitwise the same q -- with about a quarter of the
+// shared-memory load instructions (the stencil phases were bound by those,
+// profiles/r01/ncu_k_sb_persistent_c3.txt).
+template <int R, int D>
+struct PairMode {
+  using G = TileGeo<R, D>;
+  static constexpr bool kOn = (D % 2 == 0) && (G::NV * D == 4 * G::NT) && (G::TH % 2 == 0);
+  static constexpr int CP = D / 2;  // column pairs per pixel
+  static constexpr int V = kOn ? 2 : G::V;  // columns a thread accumulates (partial sums)
+};
+
+// forward slot of offset (dy, dx) (dy > 0, or dy == 0 and dx > 0)
+template <int R>
+__host__ __device__ constexpr int fwd_slot(int dy, int dx) {
+  return dy == 0 ? dx - 1 : R + (dy - 1) * (2 * R + 1) + (dx + R);
+}
+
+// The thread's pixel pair: f(tv, hpos, v, c0, q[2], pv[2]) for each pixel of
+// the pair inside the image, q = (A p)_v and pv = p_v for columns c0, c0 + 1.
+template <int R, int D, class F>
+__device__ __forceinline__ void for_tile_pairs(const Grid<R>& g, TileIdx ti, const double* P, const double* Ct,
+                                               const double* Dg, F&& f) {
+  using G = TileGeo<R, D>;
+  constexpr int CP = PairMode<R, D>::CP;
+  constexpr int WS = 2 * R + 1;
+  const int c0 = (threadIdx.x % CP) * 2;
+  const int pi = threadIdx.x / CP;
+  const int tx = pi % G::TW, tyA = (pi / G::TW) * 2;
+  const int x = ti.x0 + tx, yA = ti.y0 + tyA;
+  if (x >= g.W || yA >= g.row_hi) return;
+  const bool hasB = yA + 1 < g.row_hi;
+  const int cA = (tyA + R) * G::HW + (tx + R), cB = cA + G::HW;  // centres (halo positions)
+  double qa0 = 0.0, qa1 = 0.0, qb0 = 0.0, qb1 = 0.0;
+  double2 pa{}, pb{};
+#pragma unroll
+  for (int wr = 0; wr <= 2 * R + 1; ++wr) {
+    double2 row[WS];
+#pragma unroll
+    for (int wc = 0; wc < WS; ++wc)
+      row[wc] = *reinterpret_cast<const double2*>(P + ((tyA + wr) * G::HW + tx + wc) * D + c0);
+    // pixel A: window row wr = offset dy = wr - R; pixel B: dy = wr - 1 - R
+#pragma unroll
+    for (int who = 0; who < 2; ++who) {
+      const int dy = who == 0 ? wr - R : wr - 1 - R;
+      if (dy < -R || dy > R) continue;
+      const int cpos = who == 0 ? cA : cB;
+      double& q0 = who == 0 ? qa0 : qb0;
+      double& q1 = who == 0 ? qa1 : qb1;
+#pragma unroll
+      for (int wc = 0; wc < WS; ++wc) {
+        const int dx = wc - R;
+        const double2 pv = row[wc];
+        if (dy == 0 && dx == 0) {  // the diagonal
+          const double dg = Dg[(tyA + who) * G::TW + tx];
+          q0 = q0 + dg * pv.x;
+          q1 = q1 + dg * pv.y;
+          if (who == 0) pa = pv; else pb = pv;
+          continue;
+        }
+        const bool bwd = dy < 0 || (dy == 0 && dx < 0);
+        const int s = bwd ? fwd_slot<R>(-dy, -dx) : fwd_slot<R>(dy, dx);
+        const int npos = cpos + dy * G::HW + dx;
+        const double cw = Ct[(bwd ? npos : cpos) * G::S + s];
+        const bool nz = __double_as_longlong(cw) < 0;
+        const double t0 = cw * pv.x, t1 = cw * pv.y;
+        q0 = nz ? q0 + t0 : q0;
+        q1 = nz ? q1 + t1 : q1;
+      }
+    }
+  }
+  {
+    const double q[2] = {qa0, qa1}, pv[2] = {pa.x, pa.y};
+    f(tyA * G::TW + tx, cA, static_cast<long>(yA) * g.W + x, c0, q, pv);
+  }
+  if (hasB) {
+    const double q[2] = {qb0, qb1}, pv[2] = {pb.x, pb.y};
+    f((tyA + 1) * G::TW + tx, cB, static_cast<long>(yA + 1) * g.W + x, c0, q, pv);
+  }
+}
+
+// PCG init of one staged tile (pcg.cpp:49-66): r = b - A x0, z = D^-1 r,
+// partial sums of b.b, r.r, r.z per column.
+template <int R, int D, int V>
+__device__ __forceinline__ void tile_init_body(const Grid<R>& g, TileIdx ti, const double* P, const double* Wt,
+                                               const double* Bv, const double* Dg, const double* Iv, double* r_out,
+                                               double* z_out, double (&acc)[3][V]) {
+  if constexpr (PairMode<R, D>::kOn) {
+    for_tile_pairs<R, D>(g, ti, P, Wt, Dg, [&](int tv, int, long v, int c0, const double (&q)[2], const double (&)[2]) {
+      const double2 b = *reinterpret_cast<const double2*>(Bv + tv * D + c0);
+      const double iv = Iv[tv];
+      const double r0 = b.x - q[0], r1 = b.y - q[1];
+      const double z0 = iv * r0, z1 = iv * r1;
+      *reinterpret_cast<double2*>(r_out + v * D + c0) = make_double2(r0, r1);
+      *reinterpret_cast<double2*>(z_out + v * D + c0) = make_double2(z0, z1);
+      acc[0][0] += b.x * b.x;
+      acc[0][1] += b.y * b.y;
+      acc[1][0] += r0 * r0;
+      acc[1][1] += r1 * r1;
+      acc[2][0] += r0 * z0;
+      acc[2][1] += r1 * z1;
+    });
+  } else {
+    for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
+      const double ax = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
+      const double b = Bv[tv * D + c];
+      const double r = b - ax;
+      const double z = Iv[tv] * r;
+      r_out[v * D + c] = r;
+      z_out[v * D + c] = z;
+      acc[0][k] += b * b;
+      acc[1][k] += r * r;
+      acc[2][k] += r * z;
+    });
+  }
+}
+
+// PCG SpMV of one staged tile (P holds p' on the halo): q = A p', p' stored
+// to pnew (unless null), partial sums of p'.q per column.
+template <int R, int D, int V>
+__device__ __forceinline__ void tile_spmv_body(const Grid<R>& g, TileIdx ti, const double* P, const double* Wt,
+                                               const double* Dg, double* q_out, double* pnew, double (&acc)[1][V]) {
+  if constexpr (PairMode<R, D>::kOn) {
+    for_tile_pairs<R, D>(g, ti, P, Wt, Dg,
+                         [&](int, int, long v, int c0, const double (&q)[2], const double (&pv)[2]) {
+                           *reinterpret_cast<double2*>(q_out + v * D + c0) = make_double2(q[0], q[1]);
+                           if (pnew) *reinterpret_cast<double2*>(pnew + v * D + c0) = make_double2(pv[0], pv[1]);
+                           acc[0][0] += pv[0] * q[0];
+                           acc[0][1] += pv[1] * q[1];
+                         });
+  } else {
+    for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
+      const double qv = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
+      const double pv = P[hpos * D + c];
+      q_out[v * D + c] = qv;
+      if (pnew) pnew[v * D + c] = pv;
+      acc[0][k] += pv * qv;
+    });
+  }
+}
+
 // ---------------------------------------------------------------- init ----
 template <int D, int R>
 __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, PcgArgs a) {
   using G = TileGeo<R, D>;
-  constexpr int V = G::V;
+  constexpr int V = PairMode<R, D>::V;
   extern __shared__ double smem[];
   double* P = smem;                  // x0 halo [NP][D]
   double* Wt = smem + G::kI_W;       // coefficients [NP][S]
@@ -270,17 +419,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
     stage_interior<R, D, 1>(g, ti, g.invd, Iv);
     cp_async_wait_all();
     __syncthreads();
-    for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-      const double ax = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
-      const double b = Bv[tv * D + c];
-      const double r = b - ax;
-      const double z = Iv[tv] * r;
-      a.r[v * D + c] = r;
-      a.pbuf[0][v * D + c] = z;
-      acc[0][k] += b * b;
-      acc[1][k] += r * r;
-      acc[2][k] += r * z;
-    });
+    tile_init_body<R, D, V>(g, ti, P, Wt, Bv, Dg, Iv, a.r, a.pbuf[0], acc);
     __syncthreads();
   }
   store_partials<3, D, V, G::NT>(a, acc, a.part_a, a.tot_a);  // reduced by the first SpMV
@@ -290,7 +429,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_init(Grid<R> g, 
 template <int D, int R>
 __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, PcgArgs a) {
   using G = TileGeo<R, D>;
-  constexpr int V = G::V;
+  constexpr int V = PairMode<R, D>::V;
   extern __shared__ double smem[];
   double* P = smem;                  // p (phase 0) or p_old -> p' in place [NP][D]
   double* Rs = smem + G::kS_Rs;      // r halo [NP][D]
@@ -331,13 +470,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
       }
       __syncthreads();
     }
-    for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int k) {
-      const double q = tile_apply_A<D, R>(P, Wt, hpos, c, Dg[tv]);
-      const double pv = P[hpos * D + c];
-      a.q[v * D + c] = q;
-      if (!first) pnew[v * D + c] = pv;
-      acc[0][k] += pv * q;
-    });
+    tile_spmv_body<R, D, V>(g, ti, P, Wt, Dg, a.q, first ? nullptr : pnew, acc);
     __syncthreads();
   }
   if (!checked && !spmv_prologue<D, G::NT>(a, cv)) return;  // block without tiles

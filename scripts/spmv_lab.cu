@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <vector>
 
 namespace {
 
@@ -103,6 +104,52 @@ __global__ void __launch_bounds__(256, MINB) v_regs4(int n, const int* __restric
     double* o = q + static_cast<long>(v) * D + c0;
     reinterpret_cast<double2*>(o)[0] = make_double2(acc[0], acc[1]);
     reinterpret_cast<double2*>(o)[1] = make_double2(acc[2], acc[3]);
+  }
+}
+
+// ---- V4: as V2, but the blocks sweep the storage order together: block b
+// takes chunks b, b + nb, ... of 64 consecutive rows, so the rows gathered
+// at any moment come from a narrow window of the breadth-first order
+// (L2-resident) instead of the whole 128 MB vector.
+template <int B, int MINB, int CHUNK>
+__global__ void __launch_bounds__(256, MINB) v_sweep4(int n, const int* __restrict__ aptr, const int* __restrict__ acol,
+                                                     const double* __restrict__ aval, const double* __restrict__ p,
+                                                     double* __restrict__ q) {
+  const long total = static_cast<long>(n) * 4;
+  constexpr int ITEMS = CHUNK * 4;
+  for (long base = static_cast<long>(blockIdx.x) * ITEMS; base < total; base += static_cast<long>(gridDim.x) * ITEMS) {
+    for (long e = base + threadIdx.x; e < base + ITEMS && e < total; e += blockDim.x) {
+      const int v = static_cast<int>(e >> 2);
+      const int c0 = static_cast<int>(e & 3) * 4;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const int b = __ldg(aptr + v), en = __ldg(aptr + v + 1);
+      int cu[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) cu[j] = b + j < en ? __ldg(acol + b + j) : -1;
+      for (int k0 = b; k0 < en; k0 += B) {
+        double g[B][4];
+        double av[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (cu[j] >= 0) {
+            ldg256(p + static_cast<long>(cu[j]) * D + c0, g[j]);
+            av[j] = __ldg(aval + k0 + j);
+          }
+        int cn[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) cn[j] = k0 + B + j < en ? __ldg(acol + k0 + B + j) : -1;
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (cu[j] >= 0)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] += av[j] * g[j][k];
+#pragma unroll
+        for (int j = 0; j < B; ++j) cu[j] = cn[j];
+      }
+      double* o = q + static_cast<long>(v) * D + c0;
+      reinterpret_cast<double2*>(o)[0] = make_double2(acc[0], acc[1]);
+      reinterpret_cast<double2*>(o)[1] = make_double2(acc[2], acc[3]);
+    }
   }
 }
 
@@ -250,6 +297,53 @@ __global__ void __launch_bounds__(256, MINB) v_ring(int n, const int* __restrict
 
 extern "C" {
 
+// Storage order built from small breadth-first clusters: grow a cluster of
+// up to C unassigned vertices by BFS from a seed, give them consecutive
+// positions, take the next seed from a FIFO of the vertices discovered next
+// to earlier clusters (so consecutive clusters stay adjacent), repeat.
+// perm[v] = storage position of vertex v.
+void lab_cluster_order(int n, const int* indptr, const int* indices, int C, int* perm) {
+  std::vector<int> fifo;
+  fifo.reserve(n);
+  std::vector<char> queued(n, 0);
+  for (int v = 0; v < n; ++v) perm[v] = -1;
+  int next = 0;
+  size_t head = 0;
+  std::vector<int> cl;
+  for (int s0 = 0; s0 < n; ++s0) {
+    if (perm[s0] >= 0) continue;
+    fifo.push_back(s0);
+    queued[s0] = 1;
+    while (head < fifo.size()) {
+      const int seed = fifo[head++];
+      if (perm[seed] >= 0) continue;
+      // grow one cluster
+      cl.clear();
+      cl.push_back(seed);
+      perm[seed] = next++;
+      for (size_t h = 0; h < cl.size() && static_cast<int>(cl.size()) < C; ++h) {
+        const int v = cl[h];
+        for (int k = indptr[v]; k < indptr[v + 1] && static_cast<int>(cl.size()) < C; ++k) {
+          const int u = indices[k];
+          if (perm[u] < 0) {
+            perm[u] = next++;
+            cl.push_back(u);
+          }
+        }
+      }
+      // the cluster's unassigned neighbours seed the next clusters
+      for (int v : cl)
+        for (int k = indptr[v]; k < indptr[v + 1]; ++k) {
+          const int u = indices[k];
+          if (perm[u] < 0 && !queued[u]) {
+            queued[u] = 1;
+            fifo.push_back(u);
+          }
+        }
+    }
+  }
+}
+
 // variant ids: 0..3 registers (B, minBlocks) = (8,2) (8,3) (4,4) (12,2);
 // 10.. ring: L in {8, 16, 24, 32} x balance
 int lab_spmv(int variant, int n, const int* aptr, const int* acol, const double* aval, const double* p, double* q,
@@ -281,6 +375,16 @@ int lab_spmv(int variant, int n, const int* aptr, const int* acol, const double*
       REGS4(5, 4, 3)
       REGS4(6, 8, 2)
       REGS4(7, 4, 4)
+#define SWEEP(id, B, M, CH)                                                          \
+  case id:                                                                           \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, v_sweep4<B, M, CH>, 256, 0);  \
+    v_sweep4<B, M, CH><<<sms * nb, 256>>>(n, aptr, acol, aval, p, q);                \
+    return nb;
+      SWEEP(20, 4, 3, 64)
+      SWEEP(21, 4, 3, 16)
+      SWEEP(22, 4, 3, 256)
+      SWEEP(23, 4, 4, 64)
+      SWEEP(24, 8, 2, 64)
       case 9:
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, v_stream, 256, 0);
         v_stream<<<sms * nb, 256>>>(n, aptr, acol, aval, p, q);

@@ -59,10 +59,22 @@ def main():
     diag = diag + dt * g.degree
     a = sp.csr_matrix((np.concatenate([vals, diag]), (np.concatenate([rows, np.arange(n)]),
                                                        np.concatenate([cols, np.arange(n)]))), shape=(n, n))
-    perm, ncomp = bfs_perm(n, a.indptr, a.indices)
+    lib = C.CDLL(str(ROOT / "scripts" / "libspmv_lab.so"))
+    order = os.environ.get("LAB_ORDER", "bfs")
+    if order.startswith("cluster"):
+        csz = int(order[7:] or 64)
+        perm = np.empty(n, np.int32)
+        ip = a.indptr.astype(np.int32)
+        ix = a.indices.astype(np.int32)
+        lib.lab_cluster_order(n, ip.ctypes.data_as(C.c_void_p), ix.ctypes.data_as(C.c_void_p), csz,
+                              perm.ctypes.data_as(C.c_void_p))
+        ncomp = -1
+    else:
+        perm, ncomp = bfs_perm(n, a.indptr, a.indices)
     inv = np.argsort(perm)
     ap = a[inv][:, inv].tocsr()
     ap.sort_indices()
+    print(f"order {order}", flush=True)
     print(f"C5 A: n={n} nnz={ap.nnz} components={ncomp} max row={np.diff(ap.indptr).max()} "
           f"build {time.time() - t0:.1f} s", flush=True)
     dev = torch.device("cuda:0")
@@ -71,9 +83,8 @@ def main():
     aval = torch.tensor(ap.data, device=dev)
     rng = np.random.default_rng(0)
     p = torch.tensor(rng.standard_normal((n, d)), device=dev)
-    lib = C.CDLL(str(ROOT / "scripts" / "libspmv_lab.so"))
     lib.lab_spmv.restype = C.c_int
-    variants = [int(x) for x in sys.argv[1:]] or [0, 1, 2, 3, 5, 6, 7, 14, 9]
+    variants = [int(x) for x in sys.argv[1:]] or [0, 5, 20, 21, 22, 23, 24, 9]
     ref = None
     alg = 16 * n * d + 24 * (ap.nnz - n) // 2 + 12 * n
     for var in variants:
