@@ -339,8 +339,33 @@ def test_state_roundtrip_and_split_bregman_on_state():
         assert np.abs(getattr(st, k) - exp[k]).max() <= 1e-10, k
 
 
+def record_parity(name, g, prm, y, exp, pcg_gpu, pcg_oracle, k):
+    """Measured parity of a full-size configuration against the oracle
+    (north_star gates), printed and written to gpurun_out/full_parity_<name>.json."""
+    import json
+    from pathlib import Path
+
+    err = rel_fro_signed(y, exp)
+    o1, o2 = api.objective(g, y), O.objective(g, exp)
+    agree = label_agreement(api.kmeans(y, k, 0), O.kmeans(exp, k, 0))
+    mism = int(np.sum(np.asarray(pcg_gpu) != np.asarray(pcg_oracle)))
+    rec = {"config": name, "n": g.n, "m": g.m, "d": prm.dim, "inner": int(len(pcg_oracle)),
+           "rel_err": {"fro": err, "objective": abs(o1 - o2) / abs(o2)}, "objective_gpu": o1,
+           "objective_oracle": o2, "label_agreement": agree, "pcg_log_mismatches": mism,
+           "pcg_iterations_gpu": int(np.sum(pcg_gpu)), "pcg_iterations_oracle": int(np.sum(pcg_oracle))}
+    print(json.dumps(rec))
+    out = Path(__file__).resolve().parents[1] / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    (out / f"full_parity_{name}.json").write_text(json.dumps(rec, indent=1))
+    assert err <= 1e-6
+    assert abs(o1 - o2) <= 1e-6 * abs(o2)
+    assert agree >= 0.999
+    return rec
+
+
 def test_knn_c1_full_size_parity():
-    """BASELINE config C1 at full size: Y, objective and labels vs the oracle."""
+    """BASELINE config C1 at full size: Y, objective, labels and the PCG log
+    vs the oracle."""
     cfg = make_config("c1")
     g, prm = cfg.graph, cfg.params
     y0 = api.random_embedding(g.n, prm.dim, cfg.y0_seed, g.degree)
@@ -348,29 +373,31 @@ def test_knn_c1_full_size_parity():
     st = s.make_state(y0)
     s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
     y = st.y
-    exp = O.solve(g, prm, y0, mode=0)
-    assert rel_fro_signed(y, exp) <= 1e-6
-    assert abs(api.objective(g, y) - O.objective(g, exp)) <= 1e-6 * abs(O.objective(g, exp))
-    assert label_agreement(api.kmeans(y, cfg.k, 0), O.kmeans(exp, cfg.k, 0)) >= 0.999
+    its, _, _ = s.pcg_log()
+    res = O.solve(g, prm, y0, mode=0, log_cap=1000)
+    rec = record_parity("c1", g, prm, y, res["y"], its.max(axis=1), res["pcg_log"], cfg.k)
+    assert rec["pcg_log_mismatches"] == 0
 
 
 @pytest.mark.slow
 def test_c2_full_size_parity():
-    """BASELINE config C2 (481x321, d=4, 10x20, Jacobi tol 1e-6) vs the oracle."""
+    """BASELINE config C2 (481x321, d=4, 10x20, Jacobi tol 1e-6) vs the oracle:
+    Y, objective, labels and the PCG log."""
     cfg = make_config("c2")
     g, prm = cfg.graph, cfg.params
     y0 = api.random_embedding(g.n, prm.dim, cfg.y0_seed, g.degree)
-    got = api.soc(g, prm, y0)
+    s = api.PfeSolver(g, prm, warn=False)
+    st = s.make_state(y0)
+    s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
+    got = st.y
+    its, _, _ = s.pcg_log()
     O.set_threads(4)
     try:
         res = O.solve(g, prm, y0, mode=0, log_cap=1000)
     finally:
         O.set_threads(1)
-    exp = res["y"]
-    assert rel_fro_signed(got, exp) <= 1e-6
-    o1, o2 = api.objective(g, got), O.objective(g, exp)
-    assert abs(o1 - o2) <= 1e-6 * abs(o2)
-    assert label_agreement(api.kmeans(got, cfg.k, 0), O.kmeans(exp, cfg.k, 0)) >= 0.999
+    rec = record_parity("c2", g, prm, got, res["y"], its.max(axis=1), res["pcg_log"], cfg.k)
+    assert rec["pcg_log_mismatches"] == 0
 
 
 def test_pcg_iteration_log_matches_oracle():
