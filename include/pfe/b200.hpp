@@ -17,6 +17,7 @@
 // accessors (rows(), cols(), data(), operator()(i, j)).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -453,7 +454,29 @@ class PcgOperator {
     if (a_.nrows != a_.ncols) throw ConfigError("PcgOperator: matrix not square");
     if (cfg_.rel_tol <= 0.0) throw ConfigError("PcgOperator: rel_tol must be > 0");
     if (cfg_.max_iter < 1) throw ConfigError("PcgOperator: max_iter must be >= 1");
+    // the IC(0) breakdown test of the reference constructor (pcg.cpp:22-28),
+    // so jacobi_fallback() is known before any solve
+    if (cfg_.preconditioner == Preconditioner::Ic0) {
+      int32_t fb = 0;
+      detail::check(pfe_ic0_probe(a_.nrows, a_.row_ptr.data(), a_.col_idx.data(), a_.values.data(), &fb));
+      fallback_ = fb != 0;
+    }
   }
+
+  // PcgOperator::solve (pcg.cpp:40-92): one right-hand side.
+  std::pair<Vector, PcgReport> solve(const Vector& b, const Vector& x0) const {
+    if (b.size() != a_.nrows || x0.size() != a_.nrows) throw ConfigError("pcg_solve: dimension mismatch");
+    Matrix bm = detail::make_matrix<Matrix>(b.size(), 1), xm = detail::make_matrix<Matrix>(b.size(), 1);
+    std::copy(b.data(), b.data() + b.size(), bm.data());
+    std::copy(x0.data(), x0.data() + x0.size(), xm.data());
+    auto res = solve_multi(bm, xm);
+    Vector x(b.size());
+    std::copy(res.first.data(), res.first.data() + b.size(), x.data());
+    return {x, res.second[0]};
+  }
+
+  // pcg.hpp: true if IC(0) broke down and Jacobi is used instead.
+  bool jacobi_fallback() const { return fallback_; }
 
   std::pair<Matrix, std::vector<PcgReport>> solve_multi(const Matrix& b, const Matrix& x0) const {
     if (b.rows() != a_.nrows || x0.rows() != a_.nrows || b.cols() != x0.cols())
@@ -478,7 +501,14 @@ class PcgOperator {
   CsrMatrix a_;
   PcgConfig cfg_;
   ExecOptions x_;
+  bool fallback_ = false;
 };
+
+// pcg_solve (pcg.cpp:116-121): an operator for this call, one right-hand side.
+inline std::pair<Vector, PcgReport> pcg_solve(const CsrMatrix& a, const Vector& b, const Vector& x0,
+                                              const PcgConfig& cfg) {
+  return PcgOperator(a, cfg).solve(b, x0);
+}
 
 inline std::pair<Matrix, std::vector<PcgReport>> pcg_solve_multi(const CsrMatrix& a, const Matrix& b,
                                                                  const Matrix& x0, const PcgConfig& cfg) {

@@ -581,12 +581,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
         const double* Rq = P + G::kB_Rq;
         const double* Bo = P + G::kB_Bo;
         const TileIdx ti = tile_of<R, D>(g, t);
-        for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
-          bad |= !isfinite(P[hpos * D + c]);
-          const double acc = tile_sb_element<D, R, false>(g, P, Wt, Bo, b_old, b_new, s_out, a.gamma, hpos, c, v,
-                                                       ti.y0 + hpos / G::HW - R, ti.x0 + hpos % G::HW - R);
-          if (rhs_out) rhs_out[v * D + c] = a.hl * acc + Rq[tv * D + c];
-        });
+        bad |= tile_sb_body<D, R, false>(g, ti, P, Wt, Bo, Rq, b_old, b_new, s_out, rhs_out, a.hl, a.gamma);
         if (bulk) fence_proxy_async();  // zero-fill stores before later async writes
         __syncthreads();
         if constexpr (kDB) buf ^= 1;

@@ -542,6 +542,111 @@ __device__ __forceinline__ double tile_sb_element(const Grid<R>& g, const double
   return acc;
 }
 
+// Column-pair form of tile_sb_element (even D): one pixel, columns c0 and
+// c0 + 1, every shared / global access 16 bytes wide (half the load and
+// store instructions of two elements).  The same operations per column, in
+// the same order, so b', s and the rhs are bitwise those of
+// tile_sb_element.  b_old is loaded for a group of incident edges at a time
+// (all 2S edges in two groups for 8-neighbour grids, four groups of 6 for
+// 5x5 grids), each group's loads issued before its first use.
+template <int D, int R, bool kNc>
+__device__ __forceinline__ double2 tile_sb_pair(const Grid<R>& g, const double* P, const double* Wt, const double* Bo,
+                                                const double* __restrict__ b_old, double* b_new, double* s_out,
+                                                double gamma, int hpos, int c0, long v, int vy, int vx) {
+  using G = TileGeo<R, D>;
+  using T = GridTopo<R>;
+  double acc0 = 0.0, acc1 = 0.0;
+  const double2 pself = *reinterpret_cast<const double2*>(P + hpos * D + c0);
+  // edge e = 0 .. 2S-1 in edge order: backward slots S-1..0, then forward
+  // slots 0..S-1; b_old of a group of GS edges is loaded before its first use
+  constexpr int GS = G::S > 6 ? G::S / 2 : G::S;
+#pragma unroll
+  for (int e0 = 0; e0 < 2 * G::S; e0 += GS) {
+    double2 bo[GS];
+#pragma unroll
+    for (int i = 0; i < GS; ++i) {
+      const int e = e0 + i;
+      const bool fwd = e >= G::S;
+      const int s = fwd ? e - G::S : G::S - 1 - e;
+      const int opos = fwd ? hpos : hpos - T::dy(s) * G::HW - T::dx(s);
+      bo[i] = make_double2(0.0, 0.0);
+      const bool valid = G::kStageB ? Wt[opos * G::S + s] != 0.0
+                                    : (fwd || (vy - T::dy(s) >= 0 && vx - T::dx(s) >= 0 && vx - T::dx(s) < g.W));
+      if (b_old && valid) {
+        if constexpr (G::kStageB) {
+          bo[i] = *reinterpret_cast<const double2*>(Bo + (opos * G::S + s) * D + c0);
+        } else {
+          const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
+          const double2* src = reinterpret_cast<const double2*>(b_old + slot * D + c0);
+          bo[i] = kNc ? __ldg(src) : *src;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < GS; ++i) {
+      const int e = e0 + i;
+      const bool fwd = e >= G::S;
+      const int s = fwd ? e - G::S : G::S - 1 - e;
+      const int npos = fwd ? hpos + T::dy(s) * G::HW + T::dx(s) : hpos - T::dy(s) * G::HW - T::dx(s);
+      const int opos = fwd ? hpos : npos;  // owner = first endpoint i
+      const double w = Wt[opos * G::S + s];
+      if (w == 0.0) continue;
+      const double nw = -w;
+      const double2 pn = *reinterpret_cast<const double2*>(P + npos * D + c0);
+      const double2 pi = fwd ? pself : pn, pj = fwd ? pn : pself;
+      const double my0 = w * pi.x + nw * pj.x, my1 = w * pi.y + nw * pj.y;
+      const double sh0 = shrink1(my0 + bo[i].x, gamma), sh1 = shrink1(my1 + bo[i].y, gamma);
+      const double bn0 = bo[i].x + (my0 - sh0), bn1 = bo[i].y + (my1 - sh1);
+      const double cf = fwd ? w : nw;
+      acc0 += cf * (sh0 - bn0);
+      acc1 += cf * (sh1 - bn1);
+      if (fwd || vy - T::dy(s) < g.row_lo) {
+        const long slot = fwd ? v * G::S + s : (v - T::dy(s) * g.W - T::dx(s)) * G::S + s;
+        *reinterpret_cast<double2*>(b_new + slot * D + c0) = make_double2(bn0, bn1);
+        if (s_out) *reinterpret_cast<double2*>(s_out + slot * D + c0) = make_double2(sh0, sh1);
+      }
+    }
+  }
+  return make_double2(acc0, acc1);
+}
+
+// The split-Bregman pass over one staged tile (solver.cpp:83-84, 96-98):
+// column pairs for even D, elements otherwise.  Returns nonzero if a Y
+// value of the tile is not finite (solver.cpp:94).
+template <int D, int R, bool kNc>
+__device__ __forceinline__ int tile_sb_body(const Grid<R>& g, TileIdx ti, const double* P, const double* Wt,
+                                            const double* Bo, const double* Rq, const double* __restrict__ b_old,
+                                            double* b_new, double* s_out, double* rhs_out, double hl, double gamma) {
+  using G = TileGeo<R, D>;
+  int bad = 0;
+  if constexpr (D % 2 == 0) {
+    constexpr int CP = D / 2;
+    for (int it = threadIdx.x; it < G::NV * CP; it += G::NT) {
+      const int tv = it / CP, c0 = (it - tv * CP) * 2;
+      const int ty = tv / G::TW, tx = tv - ty * G::TW;
+      const int y = ti.y0 + ty, x = ti.x0 + tx;
+      if (y >= g.row_hi || x >= g.W) continue;
+      const int hpos = (ty + R) * G::HW + (tx + R);
+      const long v = static_cast<long>(y) * g.W + x;
+      const double2 pv = *reinterpret_cast<const double2*>(P + hpos * D + c0);
+      bad |= !isfinite(pv.x) || !isfinite(pv.y);
+      const double2 acc = tile_sb_pair<D, R, kNc>(g, P, Wt, Bo, b_old, b_new, s_out, gamma, hpos, c0, v, y, x);
+      if (rhs_out) {
+        const double2 rq = *reinterpret_cast<const double2*>(Rq + tv * D + c0);
+        *reinterpret_cast<double2*>(rhs_out + v * D + c0) = make_double2(hl * acc.x + rq.x, hl * acc.y + rq.y);
+      }
+    }
+  } else {
+    for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
+      bad |= !isfinite(P[hpos * D + c]);
+      const double acc = tile_sb_element<D, R, kNc>(g, P, Wt, Bo, b_old, b_new, s_out, gamma, hpos, c, v,
+                                                    ti.y0 + hpos / G::HW - R, ti.x0 + hpos % G::HW - R);
+      if (rhs_out) rhs_out[v * D + c] = hl * acc + Rq[tv * D + c];
+    });
+  }
+  return bad;
+}
+
 // The pass over a tile grid (tile_sb_element per element).
 template <int D, int R>
 __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, SbArgs a) {
@@ -564,12 +669,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_sb_pass(Grid<R> g, S
     }
     cp_async_wait_all();
     __syncthreads();
-    for_tile_elements<R, D>(g, ti, [&](int tv, int c, int hpos, long v, int) {
-      bad |= !isfinite(P[hpos * D + c]);
-      const double acc = tile_sb_element<D, R, true>(g, P, Wt, Bo, a.b_old, a.b_new, a.s_out, a.gamma, hpos, c, v,
-                                                          ti.y0 + hpos / G::HW - R, ti.x0 + hpos % G::HW - R);
-      if (a.rhs) a.rhs[v * D + c] = a.hl * acc + Rq[tv * D + c];
-    });
+    bad |= tile_sb_body<D, R, true>(g, ti, P, Wt, Bo, Rq, a.b_old, a.b_new, a.s_out, a.rhs, a.hl, a.gamma);
     __syncthreads();
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.ctl->nonfinite_y, 1);

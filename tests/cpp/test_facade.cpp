@@ -158,6 +158,24 @@ int main() {
     pfe::PcgConfig bad;
     bad.rel_tol = 0.0;
     CHECK(throws<pfe::ConfigError>([&] { pfe::PcgOperator(eye, bad); }));
+    // PcgOperator::solve / pcg_solve (one right-hand side, pcg.hpp:131-158)
+    pfe::Vector bv(3), xv0(3);
+    bv[0] = 0.3;
+    bv[1] = -1.0;
+    bv[2] = 2.0;
+    const pfe::PcgOperator op(eye, cfg);
+    auto [xs, rs] = op.solve(bv, xv0);
+    CHECK(rs.converged && rs.iterations <= 1 && std::abs(xs[1] + 1.0) < 1e-12);
+    auto [xf, rf] = pfe::pcg_solve(eye, bv, xv0, cfg);
+    CHECK(rf.converged && std::abs(xf[0] - 0.3) < 1e-12);
+    CHECK(!op.jacobi_fallback());
+    // the default IC(0): the constructor's breakdown test (pcg.cpp:22-28) on
+    // an SPD matrix keeps IC(0)
+    pfe::PcgConfig ic;
+    const pfe::PcgOperator op_ic(eye, ic);
+    CHECK(!op_ic.jacobi_fallback());
+    auto [xi, ri] = op_ic.solve(bv, xv0);
+    CHECK(ri.converged && std::abs(xi[2] - 2.0) < 1e-12);
   }
   std::printf("%s (%d failures)\n", failures ? "FACADE TEST FAILED" : "facade test passed", failures);
   // GMM initial embedding (init.hpp: gmm_fit + init_embedding) on the GPU:
