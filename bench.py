@@ -153,7 +153,8 @@ def ncu_traffic(config, kernel):
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(config, {}).get(kernel)
+        row = json.loads(p.read_text()).get(config, {})
+        return row.get(kernel, row.get(kernel[2:] if kernel.startswith("k_") else kernel))
     except Exception:
         return None
 

@@ -65,7 +65,7 @@ def main():
 
             os.environ["PFE_TMA"] = os.environ.get("PFE_TMA_MASK", "1")
             g, _ = image(37, 70, 1)
-            _, kind = run(g, prm(8), 2)
+            _, kind = run(g, prm(int(os.environ.get("PFE_SAN_D", "8"))), 2)
             os.environ.pop("PFE_TMA")
         elif c == "tiled24":
             g, _ = image(33, 64, 2)
