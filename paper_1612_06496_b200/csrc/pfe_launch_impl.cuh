@@ -91,15 +91,23 @@ inline bool encode_rows(CUtensorMap* m, const void* base, int K, int W, int H, i
 }
 
 // Phases of the persistent kernel that stage with TMA (PersistArgs::tma
-// bits; 16: also the one-wide arrays diag / inv diag).  Default: every phase
-// for 5x5 grids; 8-neighbour grids keep cp.async (their TMA staging faults
-// with an illegal-instruction error on B200 that is not understood yet, see
-// DESIGN.md).  PFE_TMA=0 forces cp.async everywhere (A/B tests), PFE_TMA=1
-// every phase, PFE_TMA=<mask> selects phases.
+// bits: 1 init, 2 SpMV, 4 split-Bregman, 8 b_old, 16 the one-wide arrays
+// diag / inv diag).  PFE_TMA=0 forces cp.async everywhere (A/B tests),
+// PFE_TMA=1 every phase, PFE_TMA=<mask> selects phases.
+//
+// Bit 16 is never set for odd R.  Root cause of the round-1 "illegal
+// instruction" on 8-neighbour grids (scripts/tma_probe.cu, run case by case
+// on B200): a 2-D box of a one-wide fp64 array whose first column is odd
+// starts at an 8-byte but not 16-byte aligned global address, and the TMA
+// unit faults; 3-D boxes of even row width are always 16-byte aligned.  The
+// halo box of inv diag starts at column x0 - R (x0 a multiple of 32), odd
+// for R = 1, so those arrays stay on cp.async there.
 inline int tma_mask(int radius) {
   const char* e = std::getenv("PFE_TMA");
-  if (!e || !e[0]) return radius == 2 ? 31 : 0;
-  return std::atoi(e) == 1 ? 31 : std::atoi(e);
+  int m = radius == 2 ? 31 : 0;
+  if (e && e[0]) m = std::atoi(e) == 1 ? 31 : std::atoi(e);
+  if (radius % 2 != 0) m &= ~16;
+  return m;
 }
 
 template <int D>
@@ -155,6 +163,23 @@ struct Impl {
     k_grid_sb_pass<D, R><<<grid, G::NT, sm_bytes, l.stream>>>(g, a); PFE_LAUNCHED(__func__);
   }
 
+  // General-graph (CSR) gather kernels sweep the storage order in
+  // grid-stride chunks (row_range); that is a sweep of one window only if
+  // every block is resident at once, so their grid is capped at the
+  // resident block count (SMs x occupancy).  With more blocks, the first
+  // resident wave would walk its chunks over the whole vertex range before
+  // later blocks start, and the gathered rows would miss L2.
+  template <auto Kern>
+  static int csr_grid(Launch l) {
+    static PerDeviceValue cache;  // one value per kernel instantiation and device
+    const int per_sm = static_cast<int>(cache.get([&]() -> long {
+      int nb = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, Kern, kBlock, 0);
+      return nb < 1 ? 1 : nb;
+    }));
+    return std::max(1, std::min(l.grid, per_sm * l.sm));
+  }
+
   static void pcg_grids(const TopoDesc& t, Launch l, int* nb_init, int* nb_spmv, int* nb_update) {
     *nb_update = l.grid;
     if (t.kind == kTopoGrid1) {
@@ -166,25 +191,26 @@ struct Impl {
       *nb_init = tiled_grid<2, k_grid_pcg_init<D, 2>>(sizeof(double) * G::kInit, t.g2, l.sm);
       *nb_spmv = tiled_grid<2, k_grid_pcg_spmv<D, 2>>(sizeof(double) * G::kSpmv, t.g2, l.sm);
     } else {
-      *nb_init = *nb_spmv = l.grid;
+      *nb_init = csr_grid<k_pcg_init<D, Csr>>(l);
+      *nb_spmv = csr_grid<k_pcg_spmv<D, Csr>>(l);
     }
   }
   static void pcg_init(const TopoDesc& t, const PcgArgs& a, Launch l) {
     if (t.kind == kTopoGrid1) return grid_init<1>(t.g1, a, l);
     if (t.kind == kTopoGrid2) return grid_init<2>(t.g2, a, l);
-    k_pcg_init<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+    k_pcg_init<D, Csr><<<csr_grid<k_pcg_init<D, Csr>>(l), kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void pcg_spmv(const TopoDesc& t, const PcgArgs& a, Launch l) {
     if (t.kind == kTopoGrid1) return grid_spmv<1>(t.g1, a, l);
     if (t.kind == kTopoGrid2) return grid_spmv<2>(t.g2, a, l);
     if (a.phase != 0 && !a.skip_pdir) {
-      k_pcg_pdir<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+      k_pcg_pdir<D, Csr><<<csr_grid<k_pcg_pdir<D, Csr>>(l), kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
     }
-    k_pcg_spmv<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+    k_pcg_spmv<D, Csr><<<csr_grid<k_pcg_spmv<D, Csr>>(l), kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void pcg_pdir(const TopoDesc& t, const PcgArgs& a, Launch l) {
     if (t.kind != kTopoCsr) throw std::runtime_error("pcg_pdir: CSR topologies only");
-    k_pcg_pdir<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+    k_pcg_pdir<D, Csr><<<csr_grid<k_pcg_pdir<D, Csr>>(l), kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void pack_rows(const double* src, const int* rows, int cnt, double* dst, cudaStream_t s) {
     if (cnt <= 0) return;
@@ -203,7 +229,7 @@ struct Impl {
   static void sb_pass(const TopoDesc& t, const SbArgs& a, Launch l) {
     if (t.kind == kTopoGrid1) return grid_sb<1>(t.g1, a, l);
     if (t.kind == kTopoGrid2) return grid_sb<2>(t.g2, a, l);
-    k_sb_pass<D, Csr><<<l.grid, kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
+    k_sb_pass<D, Csr><<<csr_grid<k_sb_pass<D, Csr>>(l), kBlock, 0, l.stream>>>(t.csr, a); PFE_LAUNCHED(__func__);
   }
   static void rhs_from_state(const TopoDesc& t, const double* s, const double* b, const double* rq, double* rhs,
                              double hl, Launch l) {

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -50,19 +51,22 @@ __global__ void k_probe(const __grid_constant__ CUtensorMap m, int x, int y, int
   for (int i = threadIdx.x; i < count; i += blockDim.x) out[i] = dst[i];
 }
 
-int main() {
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q{};
-  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
-    std::printf("no cuTensorMapEncodeTiled\n");
-    return 1;
-  }
-  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+int main(int argc, char** argv) {
+  // argv[1]: run only case i (a fault kills the context, so the driver
+  // script runs every case in its own process); "count": print the count
   const int H = 64, W = 96;
   struct Case {
     int K, bw, bh, x, y, dst_off;
   };
   std::vector<Case> cases;
+  for (int K : {1, 2, 4, 8})
+    for (int bw : {32, 33, 34, 35, 36, 38, 40})
+      cases.push_back({K, bw, 6, -1, -1, 0});
+  // box heights 1..16 (2-D and 3-D) and the interior boxes of the tiles
+  for (int K : {1, 4, 8})
+    for (int bh = 1; bh <= 16; ++bh) cases.push_back({K, 32, bh, 0, 0, 0});
+  for (int K : {1, 4, 8})
+    for (int bh : {4, 8}) cases.push_back({K, 32, bh, 32, 16, 0});
   for (int K : {1, 4, 8, 12, 32})
     for (int R : {1, 2})
       for (int TH : {4, 8}) {
@@ -74,6 +78,19 @@ int main() {
         }
         cases.push_back({K, bw, bh, -R, -R, 16 * 27});  // a non-zero 128-byte aligned destination offset
       }
+  if (argc > 1 && std::string(argv[1]) == "count") {
+    std::printf("%zu\n", cases.size());
+    return 0;
+  }
+  const int only = argc > 1 ? std::atoi(argv[1]) : -1;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+    std::printf("no cuTensorMapEncodeTiled\n");
+    return 1;
+  }
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+
   std::vector<double> host(static_cast<size_t>(H) * W * 32);
   for (size_t i = 0; i < host.size(); ++i) host[i] = 1.0 + static_cast<double>(i);
   double *dsrc = nullptr, *dout = nullptr;
@@ -82,7 +99,9 @@ int main() {
   cudaFuncSetAttribute(k_probe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_probe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   int fails = 0;
-  for (const Case& c : cases) {
+  for (size_t ci = 0; ci < cases.size(); ++ci) {
+    if (only >= 0 && static_cast<int>(ci) != only) continue;
+    const Case& c = cases[ci];
     cudaMemcpy(dsrc, host.data(), sizeof(double) * H * W * c.K, cudaMemcpyHostToDevice);
     CUtensorMap m;
     const cuuint32_t es[3] = {1, 1, 1};

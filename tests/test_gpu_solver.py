@@ -215,22 +215,24 @@ def test_tiled_persistent_tma_staging_bitwise(h, w, radius, d, monkeypatch):
     prm = jacobi(d, soc=2, sb=5)
     y0 = api.random_embedding(g.n, d, 2, g.degree)
     out = {}
-    for flag in ("1", "0"):
-        if flag == "1":  # TMA boxes (5x5 grids, default) / bulk row copies (8-neighbour, PFE_BULK=1)
-            monkeypatch.delenv("PFE_TMA", raising=False)
-            monkeypatch.setenv("PFE_BULK", "1")
-        else:  # per-element cp.async
-            monkeypatch.setenv("PFE_TMA", "0")
-            monkeypatch.setenv("PFE_BULK", "0")
+    # staging variants: TMA boxes (5x5 default; every phase for 8-neighbour
+    # grids with PFE_TMA=1, whose inv-diag halo stays on cp.async), bulk row
+    # copies (PFE_BULK=1, when TMA is off), per-element cp.async
+    variants = {"tma": {"PFE_TMA": "1", "PFE_BULK": "0"}, "bulk": {"PFE_TMA": "0", "PFE_BULK": "1"},
+                "cpasync": {"PFE_TMA": "0", "PFE_BULK": "0"}}
+    for name, env in variants.items():
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         s = api.PfeSolver(g, prm, warn=False, persistent="tiled")
         st = s.make_state(y0)
         s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
         assert s.report()["persistent_kind"] == 1
-        out[flag] = (st.y, st.split_b, st.split_s)
-    for a, b in zip(out["1"], out["0"]):
-        assert np.array_equal(a, b)
+        out[name] = (st.y, st.split_b, st.split_s)
+    for name in ("tma", "bulk"):
+        for a, b in zip(out[name], out["cpasync"]):
+            assert np.array_equal(a, b), name
     exp = O.solve(g, prm, y0, mode=0)
-    assert rel_fro_signed(out["1"][0], exp) <= 1e-10
+    assert rel_fro_signed(out["tma"][0], exp) <= 1e-10
 
 
 @pytest.mark.parametrize("h,w,radius,d", [(1, 200, 1, 4), (300, 4, 1, 4), (5, 300, 2, 4), (17, 6, 2, 2),
