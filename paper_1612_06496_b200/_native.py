@@ -7,11 +7,16 @@ sm_100-class GPU is present, calls fail loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpfe_b200.so"
+# A/B experiments only: PFE_LIB_VARIANT=<name> loads lib_<name>/libpfe_b200.so
+# (an in-tree build of a modified source tree, scripts/build_variant.sh)
+if os.environ.get("PFE_LIB_VARIANT"):
+    LIB_PATH = Path(__file__).resolve().parent / f"lib_{os.environ['PFE_LIB_VARIANT']}" / "libpfe_b200.so"
 
 PFE_OK, PFE_IO_ERROR, PFE_NUMERICAL_ERROR, PFE_CONFIG_ERROR, PFE_CUDA_ERROR = 0, 1, 2, 3, 4
 

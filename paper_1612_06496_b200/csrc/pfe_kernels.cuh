@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_pdir(Topo topo, PcgArgs a) {
 
 // ------------------------------------------------------- PCG SpMV (+ p update)
 template <int D, class Topo>
-__global__ void __launch_bounds__(kBlock, D == 16 ? 3 : 2) k_pcg_spmv(Topo topo, PcgArgs a) {
+__global__ void __launch_bounds__(kBlock, 2) k_pcg_spmv(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   __shared__ ColView<D> cv;
   if (!spmv_prologue<D, kBlock>(a, cv)) return;

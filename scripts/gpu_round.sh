@@ -1,16 +1,13 @@
 #!/bin/bash
-# Development round: TMA box probe (every case in its own process), GPU tests,
+# Development round: staging bitwise tests, C4 with cp.async vs TMA tiles,
 # C5 bench.
 mkdir -p gpurun_out
-n=$(./scripts/tma_probe count)
-for i in $(seq 0 $((n - 1))); do
-  timeout 30 ./scripts/tma_probe $i 2>&1 | head -1 >> gpurun_out/tma_probe_cases.log
+python -m pytest tests/test_gpu_solver.py -x -q -k "tma_staging or persistent" > gpurun_out/pytest_tma.log 2>&1
+echo "pytest tma rc=$?" >> gpurun_out/times.log
+for t in 0 1; do
+  PFE_TMA=$t python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4_tma$t.json 2> gpurun_out/bench_c4_tma$t.err
+  echo "bench c4 tma=$t rc=$?" >> gpurun_out/times.log
+  PFE_TMA=$t timeout 600 python scripts/prof_run.py c4 2 --trace > gpurun_out/trace_c4_tma$t.txt 2>&1
 done
-echo "probe cases done" >> gpurun_out/times.log
-T0=$(date +%s)
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc=$? wall=$(( $(date +%s) - T0 ))s" >> gpurun_out/times.log
-for c in ${PFE_CONFIGS:-c5}; do
-  python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
-  echo "bench $c rc=$?" >> gpurun_out/times.log
-done
+python bench.py --config c5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+echo "bench c5 rc=$?" >> gpurun_out/times.log
