@@ -280,8 +280,6 @@ template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock, 2) k_pcg_init(Topo topo, PcgArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
   double acc[3][V] = {};
-  const long total = static_cast<long>(topo.vend()) * TPV;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   long e0, e1, step;
   row_range<TPV>(topo, e0, e1, step);
   for (long e = e0; e < e1; e += step) {
@@ -338,8 +336,6 @@ __global__ void __launch_bounds__(kBlock) k_pcg_pdir(Topo topo, PcgArgs a) {
   for (int k = 0; k < V; ++k) beta[k] = cv.coef[gfirst + k];
   double* pnew = pcg_pnew(a);
   const double* pold = pcg_pold(a);
-  const long total = static_cast<long>(topo.vend()) * TPV;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   long e0, e1, step;
   row_range<TPV>(topo, e0, e1, step);
   for (long e = e0; e < e1; e += step) {
@@ -375,8 +371,6 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_spmv(Topo topo, PcgArgs a) {
   double* pnew = pcg_pnew(a);
   const double* pold = pcg_pold(a);
   double acc[1][V] = {};
-  const long total = static_cast<long>(topo.vend()) * TPV;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   long e0, e1, step;
   row_range<TPV>(topo, e0, e1, step);
   for (long e = e0; e < e1; e += step) {
@@ -554,8 +548,6 @@ struct SbArgs {
 template <int D, class Topo>
 __global__ void __launch_bounds__(kBlock, D == 16 ? 2 : 3) k_sb_pass(Topo topo, SbArgs a) {
   constexpr int V = Cols<D>::V, TPV = Cols<D>::TPV;
-  const long total = static_cast<long>(topo.vend()) * TPV;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   int bad = 0;
   long e0, e1, step;
   row_range<TPV>(topo, e0, e1, step);

@@ -88,7 +88,10 @@ struct PersistCols {
 template <int D, int R>
 struct PersistGeo {
   using G = TileGeo<R, D>;
-  static constexpr int kInit2 = 2 * G::kInit, kSpmv2 = 2 * G::kSpmv;
+  // tile buffers of the init and SpMV phases: a ring of kRing (one tile
+  // evaluated while kRing - 1 are staged)
+  static constexpr int kRing = 2;
+  static constexpr int kInit2 = kRing * G::kInit, kSpmv2 = kRing * G::kSpmv;
   static constexpr int kA = kInit2 > kSpmv2 ? kInit2 : kSpmv2;
   static constexpr int kSbB = G::kStageB ? G::kSb : 2 * G::kSb;  // sb phase (double-buffered for 5x5)
   static constexpr int kSmem = kA > kSbB ? kA : kSbB;  // doubles
@@ -122,17 +125,26 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
   PFE_TRACE(0);
   // TMA staging: one mbarrier per tile buffer; tph holds each buffer's
   // expected phase parity (identical in every thread)
-  __shared__ alignas(8) uint64_t tbar[2];
+  constexpr int NB = PersistGeo<D, R>::kRing > 2 ? PersistGeo<D, R>::kRing : 2;  // mbarriers / tile buffers
+  __shared__ alignas(8) uint64_t tbar[NB];
   const bool tma_any = a.tma != 0;
   const bool bulk_any = a.bulk != 0;
   uint32_t tph = 0;
   if ((tma_any || bulk_any) && threadIdx.x == 0) {
-    mbar_init(&tbar[0], 1);
-    mbar_init(&tbar[1], 1);
+    for (int i = 0; i < NB; ++i) mbar_init(&tbar[i], 1);
     mbar_fence_init();
   }
   __syncthreads();
   const bool bulk = a.bulk != 0;
+  // ring form for the init / SpMV phases: NR - 1 tiles staged ahead
+  constexpr int NR = PersistGeo<D, R>::kRing;
+  auto ring_wait = [&](bool tma, int buf) {
+    if (tma || bulk) {
+      mbar_wait(&tbar[buf], (tph >> buf) & 1u);
+      tph ^= 1u << buf;
+    }
+    cp_async_wait<NR - 1>();
+  };
   auto tile_wait = [&](bool tma, int buf, bool more) {
     if (tma || bulk) {
       mbar_wait(&tbar[buf], (tph >> buf) & 1u);
@@ -205,13 +217,15 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
         stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         stage_interior<R, D, 1>(g, ti, g.invd, Iv);
       };
-      int buf = 0;
-      if (blockIdx.x < nt) stage(blockIdx.x, 0);
-      cp_async_commit();
-      for (int t = blockIdx.x; t < nt; t += nb) {
-        if (t + nb < nt) stage(t + nb, buf ^ 1);
+      for (int j = 0; j < NR - 1; ++j) {
+        if (blockIdx.x + j * nb < nt) stage(blockIdx.x + j * nb, j);
         cp_async_commit();
-        tile_wait(tma, buf, true);
+      }
+      int buf = 0;
+      for (int t = blockIdx.x; t < nt; t += nb) {
+        if (t + (NR - 1) * nb < nt) stage(t + (NR - 1) * nb, (buf + NR - 1) % NR);
+        cp_async_commit();
+        ring_wait(tma, buf);
         __syncthreads();
         const double* P = smem + buf * G::kInit;
         const double* Wt = P + G::kI_W;
@@ -222,7 +236,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
         tile_init_body<R, D, V>(g, ti, P, Wt, Bv, Dg, Iv, a.r, a.pbuf[0], acc);
         if (bulk) fence_proxy_async();  // zero-fill stores before later async writes
         __syncthreads();
-        buf ^= 1;
+        buf = (buf + 1) % NR;
       }
       cp_async_wait<0>();
       block_reduce_store<3, D, V, NT>(acc, a.part);
@@ -323,13 +337,15 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
           stage_rows<R, D, G::S>(g, ti, g.cf, Wt, G::HH);
           stage_interior<R, D, 1>(g, ti, g.diag, Dg);
         };
-        int buf = 0;
-        if (blockIdx.x < nt) stage(blockIdx.x, 0);
-        cp_async_commit();
-        for (int t = blockIdx.x; t < nt; t += nb) {
-          if (t + nb < nt) stage(t + nb, buf ^ 1);
+        for (int j = 0; j < NR - 1; ++j) {
+          if (blockIdx.x + j * nb < nt) stage(blockIdx.x + j * nb, j);
           cp_async_commit();
-          tile_wait(tma, buf, true);
+        }
+        int buf = 0;
+        for (int t = blockIdx.x; t < nt; t += nb) {
+          if (t + (NR - 1) * nb < nt) stage(t + (NR - 1) * nb, (buf + NR - 1) % NR);
+          cp_async_commit();
+          ring_wait(tma, buf);
           __syncthreads();
           double* P = smem + buf * G::kSpmv;
           const double* Rs = P + G::kS_Rs;
@@ -349,7 +365,7 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT, R == 2 ? 1 : 2)
           // this buffer (async proxy) must be ordered after those writes
           if (tma || bulk) fence_proxy_async();
           __syncthreads();
-          buf ^= 1;
+          buf = (buf + 1) % NR;
         }
         cp_async_wait<0>();
         block_reduce_store<1, D, V, NT>(acc, a.part_b);

@@ -760,7 +760,43 @@ int grid_slot(int R, int W, int i, int j) {
 // Breadth-first order of the vertices (components in vertex order, neighbours
 // in incidence order): perm[v] = position of v.  Used as the storage order of
 // general graphs and as the basis of vertex-range partitions.
+// Reverse Cuthill-McKee alternative (A/B experiments, PFE_STORAGE_ORDER=rcm):
+// per component, BFS from a minimum-degree vertex with each vertex's
+// unvisited neighbours taken in ascending degree, then the whole order
+// reversed.  Aims at a smaller bandwidth than the plain BFS.
+std::vector<int> rcm_storage_order(int n, const std::vector<int>& iptr, const int* inbr) {
+  std::vector<int> perm(n, -1), order;
+  order.reserve(n);
+  std::vector<int> deg(n), byd(n);
+  for (int v = 0; v < n; ++v) deg[v] = iptr[v + 1] - iptr[v];
+  std::iota(byd.begin(), byd.end(), 0);
+  std::stable_sort(byd.begin(), byd.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+  std::vector<char> seen(n, 0);
+  std::vector<int> nb;
+  for (int s0 : byd) {
+    if (seen[s0]) continue;
+    size_t head = order.size();
+    seen[s0] = 1;
+    order.push_back(s0);
+    while (head < order.size()) {
+      const int v = order[head++];
+      nb.clear();
+      for (int k = iptr[v]; k < iptr[v + 1]; ++k)
+        if (!seen[inbr[k]]) {
+          seen[inbr[k]] = 1;
+          nb.push_back(inbr[k]);
+        }
+      std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+      order.insert(order.end(), nb.begin(), nb.end());
+    }
+  }
+  for (int i = 0; i < n; ++i) perm[order[n - 1 - i]] = i;
+  return perm;
+}
+
 std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const int* inbr) {
+  if (const char* o = std::getenv("PFE_STORAGE_ORDER"); o && std::string(o) == "rcm")
+    return rcm_storage_order(n, iptr, inbr);
   std::vector<int> perm(n, -1), queue(n);
   int next = 0, head = 0;
   for (int s0 = 0; s0 < n; ++s0) {
