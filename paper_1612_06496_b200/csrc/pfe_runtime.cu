@@ -159,9 +159,20 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
 }
 constexpr size_t kStageMin = 16u << 20;  // smaller copies go direct
 
+// Page-locked (cudaMallocHost / cudaHostRegister) host memory: the DMA
+// engine reads it directly, no bounce buffer needed.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: a plain pageable pointer is not an error
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   PinnedStage& ps = pinned_stage();
-  if (bytes < kStageMin || !ps.ready()) {
+  if (bytes < kStageMin || host_pinned(src) || !ps.ready()) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
@@ -179,7 +190,7 @@ void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 // Blocking: returns when dst holds the data.
 void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   PinnedStage& ps = pinned_stage();
-  if (bytes < kStageMin || !ps.ready()) {
+  if (bytes < kStageMin || host_pinned(dst) || !ps.ready()) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return;
@@ -457,7 +468,8 @@ struct pfe_solver {
   long m = 0;
   int d = 0;
   TopoDesc topo;
-  std::vector<long> edge_row;  // edge e -> row of the device edge arrays
+  std::vector<long> edge_row;  // edge e -> row of the device edge arrays (host copy)
+  int32_t* d_edge_slot = nullptr;  // device copy when the grid topology was built on the device
   // General graphs store vertices in a locality order (BFS): perm_h[v] = the
   // device row of vertex v (empty / null: identity).  Only storage moves; every
   // row keeps its terms in the reference's order.
@@ -572,6 +584,83 @@ namespace {
 // Off-diagonal entries of A per forward stencil slot, exactly as
 // form_normal_matrix forms them ((hl * (+w)) * (-w) == -((hl * w) * w),
 // sparse.cpp:114); +0.0 marks an absent edge (Grid::cf).
+// Grid topology on the device (pixel-grid graphs): the forward stencil slot
+// of every edge (i, j) -- exactly the host test below: lexicographic order,
+// (dy, dx) from j - i, no wrap-around -- written as slot weights wf[i*S + s]
+// and the edge -> slot map; any edge that breaks the grid contract sets
+// *bad (the host then builds the general CSR topology instead).
+__global__ void k_grid_slots(long m, int gw, int grad, const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
+                             const double* __restrict__ w, double* __restrict__ wf, int32_t* __restrict__ slot,
+                             int* __restrict__ bad) {
+  const int S_ = grad == 1 ? 4 : 12;
+  for (long k = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int i = __ldg(ei + k), j = __ldg(ej + k);
+    bool ok = true;
+    if (k > 0) {
+      const int pi = __ldg(ei + k - 1), pj = __ldg(ej + k - 1);
+      ok = pi < i || (pi == i && pj < j);
+    }
+    const long dlt = static_cast<long>(j) - i;
+    const int dy = static_cast<int>((dlt + grad) / gw);
+    const int dx = static_cast<int>(dlt - static_cast<long>(dy) * gw);
+    const int xi = i % gw;
+    int s = -1;
+    if (xi + dx >= 0 && xi + dx < gw) {
+      if (grad == 1) {
+        if (dy == 0 && dx == 1) s = 0;
+        else if (dy == 1 && dx >= -1 && dx <= 1) s = 2 + dx;
+      } else {
+        if (dy == 0 && (dx == 1 || dx == 2)) s = dx - 1;
+        else if (dy == 1 && dx >= -2 && dx <= 2) s = 4 + dx;
+        else if (dy == 2 && dx >= -2 && dx <= 2) s = 9 + dx;
+      }
+    }
+    if (!ok || s < 0) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    const int32_t row = i * S_ + s;
+    slot[k] = row;
+    wf[row] = __ldg(w + k);
+  }
+}
+
+// sqrt(d_v) (correctly rounded, as std::sqrt)
+__global__ void k_sqrt(long n, const double* __restrict__ a, double* __restrict__ out) {
+  for (long v = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += static_cast<long>(gridDim.x) * blockDim.x)
+    out[v] = sqrt(__ldg(a + v));
+}
+
+// diag(A)_v = sum over incident edges in edge-index order (backward slots,
+// u ascending, then forward slots; absent slots hold 0 and add +0.0) of
+// (hl w) w, then + (r/2) d_v last (sparse.cpp:96-122); inv diag (pcg.cpp:15-20).
+// The same operations in the same order as the host loop.
+__global__ void k_grid_diag(int gh, int gw, int grad, double hl, double dterm, int precond_none,
+                            const double* __restrict__ wf, const double* __restrict__ deg, double* __restrict__ diag,
+                            double* __restrict__ invd) {
+  const int S_ = grad == 1 ? 4 : 12;
+  const long n = static_cast<long>(gh) * gw;
+  for (long v = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(v / gw), x = static_cast<int>(v - static_cast<long>(y) * gw);
+    double acc = 0.0;
+    for (int s = S_ - 1; s >= 0; --s) {
+      const int sdy = grad == 1 ? (s == 0 ? 0 : 1) : (s < 2 ? 0 : (s < 7 ? 1 : 2));
+      const int sdx = grad == 1 ? (s == 0 ? 1 : s - 2) : (s < 2 ? s + 1 : (s < 7 ? s - 4 : s - 9));
+      const int yy = y - sdy, xx = x - sdx;
+      if (yy < 0 || xx < 0 || xx >= gw) continue;
+      const double w = wf[(v - (static_cast<long>(sdy) * gw + sdx)) * S_ + s];
+      acc += (hl * w) * w;
+    }
+    for (int s = 0; s < S_; ++s) {
+      const double w = wf[v * S_ + s];
+      acc += (hl * w) * w;
+    }
+    const double dv = acc + dterm * __ldg(deg + v);
+    diag[v] = dv;
+    invd[v] = precond_none ? 1.0 : (dv > 0.0 ? 1.0 / dv : 1.0);
+  }
+}
+
 __global__ void k_grid_coef(long cnt, const double* __restrict__ wf, double hl, double* __restrict__ cf) {
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < cnt;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -1015,6 +1104,71 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
   // the column order, edges strictly lexicographic and all stencil offsets.
   bool grid = gh > 0 && gw > 0 && static_cast<long>(gh) * gw == n && (grad == 1 || grad == 2) &&
               gw >= 2 * grad + 2;
+  if (grid && static_cast<long>(n) * (grad == 1 ? 4 : 12) < 0x7fffffffL &&
+      !(std::getenv("PFE_HOST_TOPOLOGY") && std::getenv("PFE_HOST_TOPOLOGY")[0] == '1')) {
+    // Pixel grid on the device: upload the edge list once, derive the slot
+    // weights, the edge -> slot map, diag and inv diag there (the host loop
+    // below costs ~0.4 s on C4's 67 M edges and uploads the same bytes).
+    const int S_ = grad == 1 ? 4 : 12;
+    const long ns = static_cast<long>(n) * S_;
+    DevPool tmp;
+    tmp.stream = tmp.fstream = st;
+    int32_t* d_ei = tmp.alloc<int32_t>(static_cast<size_t>(m));
+    int32_t* d_ej = tmp.alloc<int32_t>(static_cast<size_t>(m));
+    double* d_w = tmp.alloc<double>(static_cast<size_t>(m));
+    double* d_deg = S->mem.alloc<double>(static_cast<size_t>(n));  // kept: the solver's degree array
+    int* d_bad = tmp.alloc<int>(1);
+    copy_h2d(d_ei, g.ei, sizeof(int32_t) * m, st);
+    copy_h2d(d_ej, g.ej, sizeof(int32_t) * m, st);
+    copy_h2d(d_w, g.w, sizeof(double) * m, st);
+    copy_h2d(d_deg, g.deg, sizeof(double) * n, st);
+    double* dwf = S->mem.alloc<double>(static_cast<size_t>(ns));
+    int32_t* dslot = S->mem.alloc<int32_t>(static_cast<size_t>(std::max(m, 1L)));
+    CK(cudaMemsetAsync(dwf, 0, sizeof(double) * ns, st));
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    const int blocks = static_cast<int>(std::min<long>(std::max<long>(1, (m + 255) / 256), 32L * S->sm));
+    if (m > 0) k_grid_slots<<<blocks, 256, 0, st>>>(m, gw, grad, d_ei, d_ej, d_w, dwf, dslot, d_bad);
+    CK(cudaGetLastError());
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!bad) {
+      if (S->row_hi < 0) {
+        S->row_lo = 0;
+        S->row_hi = gh;
+      }
+      S->diag = S->mem.alloc<double>(static_cast<size_t>(n));
+      S->invd = S->mem.alloc<double>(static_cast<size_t>(n));
+      const int vb = static_cast<int>(std::min<long>((n + 255) / 256, 32L * S->sm));
+      k_grid_diag<<<std::max(1, vb), 256, 0, st>>>(gh, gw, grad, hl, dterm, S->prm.preconditioner == PFE_PRECOND_NONE,
+                                                   dwf, d_deg, S->diag, S->invd);
+      CK(cudaGetLastError());
+      S->d_edge_slot = dslot;
+      S->edge_rows = ns;
+      S->deg = d_deg;  // grids keep vertex order: upload_degree has nothing left to do
+      S->sqd = S->mem.alloc<double>(static_cast<size_t>(n));
+      k_sqrt<<<std::max(1, vb), 256, 0, st>>>(n, d_deg, S->sqd);
+      CK(cudaGetLastError());
+      double* dcf = grid_coef(S, dwf, ns, hl, st);
+      CK(cudaStreamSynchronize(st));  // the temporaries are freed next
+      tmp.free_all();
+      if (grad == 1) {
+        S->topo.kind = pfe_host::kTopoGrid1;
+        S->topo.g1 = pfe_dev::Grid<1>{n, gh, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+        S->topo.g1.cf = dcf;
+      } else {
+        S->topo.kind = pfe_host::kTopoGrid2;
+        S->topo.g2 = pfe_dev::Grid<2>{n, gh, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+        S->topo.g2.cf = dcf;
+      }
+      return;
+    }
+    tmp.free_all();
+    S->mem.release(dwf);
+    S->mem.release(dslot);
+    S->mem.release(d_deg);
+    grid = false;  // not a stencil graph after all: general CSR topology
+  }
   std::vector<long> slot_of;
   if (grid) {
     slot_of.resize(static_cast<size_t>(m));
@@ -1334,6 +1488,7 @@ void init_common(pfe_solver* S, const pfe_exec* x, int d) {
 
 // deg and sqrt(deg) in device row order (after build_topology chose it).
 void upload_degree(pfe_solver* S, const double* degree) {
+  if (S->deg && S->sqd) return;  // built with the device grid topology
   const int n = S->n;
   std::vector<double> deg(n), sqd(n);
   for (int v = 0; v < n; ++v) {
@@ -2046,6 +2201,18 @@ void pfe_state_destroy(pfe_state* st) {
   delete st;
 }
 
+// The edge -> device-row map on the host (state get / set of split_b and
+// split_s, edge order), downloaded on first use when the topology was
+// built on the device.
+const std::vector<long>& host_edge_rows(pfe_solver* S) {
+  if (S->edge_row.empty() && S->d_edge_slot && S->m > 0) {
+    std::vector<int32_t> t(static_cast<size_t>(S->m));
+    stream_copy(t.data(), S->d_edge_slot, sizeof(int32_t) * t.size(), cudaMemcpyDeviceToHost, S->stream);
+    S->edge_row.assign(t.begin(), t.end());
+  }
+  return S->edge_row;
+}
+
 int pfe_state_get(pfe_state* st, int32_t field, double* out) {
   return guarded([&] {
     pfe_solver* S = st->s;
@@ -2071,8 +2238,9 @@ int pfe_state_get(pfe_state* st, int32_t field, double* out) {
     const double* src = field == PFE_FIELD_SPLIT_B ? st->eb[st->eb_cur] : st->es;
     std::vector<double> rows(static_cast<size_t>(S->edge_rows) * d);
     stream_copy(rows.data(), src, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost, S->stream);
+    const std::vector<long>& er = host_edge_rows(S);
     for (long e = 0; e < m; ++e)
-      for (int j = 0; j < d; ++j) out[e + j * m] = rows[static_cast<size_t>(S->edge_row[e]) * d + j];
+      for (int j = 0; j < d; ++j) out[e + j * m] = rows[static_cast<size_t>(er[e]) * d + j];
   });
 }
 
@@ -2098,8 +2266,9 @@ int pfe_state_set(pfe_state* st, int32_t field, const double* in) {
       stream_copy(s_rows.data(), st->es, sizeof(double) * s_rows.size(), cudaMemcpyDeviceToHost, S->stream);
     }
     std::vector<double>& tgt = field == PFE_FIELD_SPLIT_B ? b_rows : s_rows;
+    const std::vector<long>& er = host_edge_rows(S);
     for (long e = 0; e < m; ++e)
-      for (int j = 0; j < d; ++j) tgt[static_cast<size_t>(S->edge_row[e]) * d + j] = in[e + j * m];
+      for (int j = 0; j < d; ++j) tgt[static_cast<size_t>(er[e]) * d + j] = in[e + j * m];
     stream_copy(st->eb[st->eb_cur], b_rows.data(), sizeof(double) * b_rows.size(), cudaMemcpyHostToDevice, S->stream);
     stream_copy(st->es, s_rows.data(), sizeof(double) * s_rows.size(), cudaMemcpyHostToDevice, S->stream);
     st->inner_zero = false;
