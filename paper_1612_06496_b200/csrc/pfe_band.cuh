@@ -6,8 +6,10 @@
 // [r0 - R, r1 + R) clipped to the image: its owned rows plus an R-row halo
 // (R = stencil radius).  Every kernel processes owned rows only (Grid::row_lo
 // / row_hi); the halo rows are copies refreshed from the neighbouring bands:
-//   * p0 after init, p' after every SpMV and r after every update (the fused
-//     SpMV recomputes p' = D^-1 r + beta p on its halo),
+//   * p0 after init and r after every update (the fused SpMV recomputes
+//     p' = D^-1 r + beta p on its halo from exchanged r and stores the halo
+//     rows of p' itself, so p' needs no exchange: one halo exchange per PCG
+//     iteration),
 //   * Y after every result selection (init and the split-Bregman pass read
 //     the neighbours' rows).
 // split_b / split_s of an edge crossing a band boundary are replicated in both
@@ -367,7 +369,8 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
   const bool ranges = t.S(0)->part == 2;
   // one PCG iteration after the SpMV of iteration k: update k, SpMV k + 1
   auto iteration = [&](int k) {
-    if (k > 1 && !ranges) team_halo(t, [k](pfe_state* st) { return (k & 1) ? st->pb[0] : st->pb[1]; });
+    // (row bands need no halo exchange of p here: the SpMV stored the halo
+    // rows of p' it formed from exchanged r, k_grid_pcg_spmv)
     for (size_t i = 0; i < B; ++i) {
       a[i].phase = pfe_dev::pcg_phase(k);
       on(t.S(i))->tab->pcg_update(t.S(i)->topo, a[i], t.S(i)->lv());

@@ -471,6 +471,26 @@ __global__ void __launch_bounds__(TileGeo<R, D>::NT) k_grid_pcg_spmv(Grid<R> g, 
       __syncthreads();
     }
     tile_spmv_body<R, D, V>(g, ti, P, Wt, Dg, a.q, first ? nullptr : pnew, acc);
+    if (!first && (g.row_lo > 0 || g.row_hi < g.H)) {
+      // Row band: the halo rows of p' above / below the band were formed in
+      // shared memory from exchanged r and the previous p (bit-identical to
+      // the neighbouring band's own p'); storing them saves the halo
+      // exchange of p before the next SpMV (pcg.cpp:86-88).
+      const int top0 = ti.y0 == g.row_lo ? max(g.row_lo - R, 0) : 0, top1 = ti.y0 == g.row_lo ? g.row_lo : 0;
+      const bool bot = ti.y0 + G::TH >= g.row_hi;
+      const int bot0 = bot ? g.row_hi : 0, bot1 = bot ? min(g.row_hi + R, g.H) : 0;
+      const int cols = min(G::TW, g.W - ti.x0);
+      for (int band = 0; band < 2; ++band) {
+        const int y0 = band == 0 ? top0 : bot0, y1 = band == 0 ? top1 : bot1;
+        const int cnt = (y1 - y0) * cols * D;
+        for (int e = threadIdx.x; e < cnt; e += G::NT) {
+          const int pix = e / D, c = e - pix * D;
+          const int y = y0 + pix / cols, x = ti.x0 + pix % cols;
+          const int hpos = (y - ti.y0 + R) * G::HW + (x - ti.x0 + R);
+          pnew[(static_cast<long>(y) * g.W + x) * D + c] = P[hpos * D + c];
+        }
+      }
+    }
     __syncthreads();
   }
   if (!checked && !spmv_prologue<D, G::NT>(a, cv)) return;  // block without tiles
