@@ -9,15 +9,18 @@
 // graph launch with no host round trips.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -103,24 +106,102 @@ void retain_pool_memory(int dev) {
   done[dev] = true;
 }
 
+// Process-wide pool of host worker threads for parallel_for: creating 16
+// std::threads per call cost ~0.5 ms, which made the many small parallel
+// loops of the general-graph set-up (one per breadth-first level) slower
+// than serial.  Workers sleep on a condition variable between jobs; one job
+// runs at a time (callers from several host threads queue on `run_mu`); a
+// parallel_for issued from inside a worker runs inline.
+struct HostPool {
+  std::mutex run_mu;  // one job at a time
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::vector<std::thread> workers;
+  const std::function<void(long, long)>* job = nullptr;
+  long n = 0, per = 0;
+  int parts = 0, next_part = 0, pending = 0;
+  unsigned long gen = 0;
+  bool stop = false;
+  static thread_local bool in_worker;
+
+  explicit HostPool(int nthreads) {
+    for (int w = 0; w < nthreads; ++w) workers.emplace_back([this] { loop(); });
+  }
+  // run part p of the current job (mu not held)
+  void run_part(int p) {
+    const long b = p * per, e = std::min(n, b + per);
+    if (b < e) (*job)(b, e);
+  }
+  void loop() {
+    in_worker = true;
+    unsigned long seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return stop || (gen != seen && next_part < parts); });
+      if (stop) return;
+      while (next_part < parts) {
+        const int p = next_part++;
+        lk.unlock();
+        run_part(p);
+        lk.lock();
+        if (--pending == 0) done_cv.notify_all();
+      }
+      seen = gen;
+    }
+  }
+  void run(long total, int t, const std::function<void(long, long)>& f) {
+    std::lock_guard<std::mutex> serial(run_mu);
+    std::unique_lock<std::mutex> lk(mu);
+    job = &f;
+    n = total;
+    parts = t;
+    per = (total + t - 1) / t;
+    next_part = 0;
+    pending = t;
+    ++gen;
+    cv.notify_all();
+    in_worker = true;  // a parallel_for inside f on this thread runs inline
+    while (next_part < parts) {  // the caller works too
+      const int p = next_part++;
+      lk.unlock();
+      run_part(p);
+      lk.lock();
+      --pending;
+    }
+    in_worker = false;
+    done_cv.wait(lk, [&] { return pending == 0; });
+    job = nullptr;
+  }
+};
+thread_local bool HostPool::in_worker = false;
+
+HostPool& host_pool() {
+  // never destroyed: workers live for the process.  A forked child has no
+  // copies of the parent's threads, so it builds its own pool.
+  static std::mutex mu;
+  static HostPool* pool = nullptr;
+  static pid_t owner = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pool || owner != getpid()) {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    pool = new HostPool(std::min(hw, 16) - 1);
+    owner = getpid();
+  }
+  return *pool;
+}
+
 // f(begin, end) over [0, n) on up to 16 host threads (chunks of >= grain
 // items; small inputs run inline).  f must not throw.
 template <class F>
 void parallel_for(long n, F&& f, long grain = 1L << 16) {
   const long hw = std::max(1u, std::thread::hardware_concurrency());
   const int t = static_cast<int>(std::min<long>(std::min<long>(hw, 16), (n + grain - 1) / std::max(1L, grain)));
-  if (t <= 1) {
+  if (t <= 1 || HostPool::in_worker) {
     f(0L, n);
     return;
   }
-  const long per = (n + t - 1) / t;
-  std::vector<std::thread> pool;
-  for (int w = 0; w < t; ++w) {
-    const long b = w * per, e = std::min(n, b + per);
-    if (b >= e) break;
-    pool.emplace_back([&f, b, e] { f(b, e); });
-  }
-  for (auto& th : pool) th.join();
+  const std::function<void(long, long)> fn = [&f](long b, long e) { f(b, e); };
+  host_pool().run(n, t, fn);
 }
 
 // Large copies between pageable host memory and the device go through two
@@ -916,7 +997,7 @@ std::vector<int> bfs_storage_order_serial(int n, const std::vector<int>& iptr, c
 std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const int* inbr) {
   if (const char* o = std::getenv("PFE_STORAGE_ORDER"); o && std::string(o) == "rcm")
     return rcm_storage_order(n, iptr, inbr);
-  constexpr long kParallelEntries = 1L << 18;  // smaller levels run serially
+  constexpr long kParallelEntries = 1L << 15;  // smaller levels run serially
   std::vector<int> perm(n, -1), queue(n);
   std::unique_ptr<std::atomic<uint64_t>[]> best(new std::atomic<uint64_t>[n]);
   for (int v = 0; v < n; ++v) best[v].store(~0ULL, std::memory_order_relaxed);
