@@ -964,8 +964,12 @@ std::vector<int> rcm_storage_order(int n, const std::vector<int>& iptr, const in
   return perm;
 }
 
-// The sequential breadth-first order (reference for bfs_storage_order).
-std::vector<int> bfs_storage_order_serial(int n, const std::vector<int>& iptr, const int* inbr) {
+// Breadth-first storage order (serial queue: a level-parallel version that
+// reproduced the same order with atomic first-visit keys measured slower on
+// C5, 217 vs 130 ms).
+std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const int* inbr) {
+  if (const char* o = std::getenv("PFE_STORAGE_ORDER"); o && std::string(o) == "rcm")
+    return rcm_storage_order(n, iptr, inbr);
   std::vector<int> perm(n, -1), queue(n);
   int next = 0, head = 0;
   for (int s0 = 0; s0 < n; ++s0) {
@@ -986,104 +990,6 @@ std::vector<int> bfs_storage_order_serial(int n, const std::vector<int>& iptr, c
   return perm;
 }
 
-// The same order, level by level with the large levels in parallel.  The
-// sequential queue appends a vertex when its FIRST visit happens, i.e. at the
-// smallest (frontier position f, offset k in that vertex's incidence list)
-// among the frontier vertices adjacent to it.  Per level: pass 1 takes the
-// minimum of the 64-bit key (f << 32 | k) per newly reached vertex (atomic
-// min); pass 2 counts each frontier vertex's winners; an exclusive scan
-// gives their positions; pass 3 writes them in incidence order.  Identical
-// to bfs_storage_order_serial (PFE_BFS_CHECK=1 compares the two).
-std::vector<int> bfs_storage_order(int n, const std::vector<int>& iptr, const int* inbr) {
-  if (const char* o = std::getenv("PFE_STORAGE_ORDER"); o && std::string(o) == "rcm")
-    return rcm_storage_order(n, iptr, inbr);
-  constexpr long kParallelEntries = 1L << 15;  // smaller levels run serially
-  std::vector<int> perm(n, -1), queue(n);
-  std::unique_ptr<std::atomic<uint64_t>[]> best(new std::atomic<uint64_t>[n]);
-  for (int v = 0; v < n; ++v) best[v].store(~0ULL, std::memory_order_relaxed);
-  std::vector<long> off;
-  int next = 0;
-  for (int s0 = 0; s0 < n; ++s0) {
-    if (perm[s0] >= 0) continue;
-    perm[s0] = next;
-    queue[next++] = s0;
-    int lo = next - 1;  // current frontier [lo, hi)
-    while (lo < next) {
-      const int hi = next;
-      long entries = 0;
-      for (int f = lo; f < hi && entries < kParallelEntries; ++f) entries += iptr[queue[f] + 1] - iptr[queue[f]];
-      if (entries < kParallelEntries) {  // small level: the sequential rule directly
-        for (int f = lo; f < hi; ++f) {
-          const int v = queue[f];
-          for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
-            const int u = inbr[k];
-            if (perm[u] < 0) {
-              perm[u] = next;
-              queue[next++] = u;
-            }
-          }
-        }
-        lo = hi;
-        continue;
-      }
-      const long nf = hi - lo;
-      parallel_for(nf, [&](long b, long e) {  // pass 1: first visit of every new vertex
-        for (long fi = b; fi < e; ++fi) {
-          const int v = queue[lo + fi];
-          for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
-            const int u = inbr[k];
-            if (perm[u] >= 0) continue;
-            const uint64_t key = (static_cast<uint64_t>(fi) << 32) | static_cast<uint32_t>(k - iptr[v]);
-            uint64_t cur = best[u].load(std::memory_order_relaxed);
-            while (key < cur && !best[u].compare_exchange_weak(cur, key, std::memory_order_relaxed)) {
-            }
-          }
-        }
-      }, 4096);
-      off.assign(static_cast<size_t>(nf) + 1, 0);
-      parallel_for(nf, [&](long b, long e) {  // pass 2: winners per frontier vertex
-        for (long fi = b; fi < e; ++fi) {
-          const int v = queue[lo + fi];
-          long c = 0;
-          for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
-            const int u = inbr[k];
-            if (perm[u] < 0 &&
-                best[u].load(std::memory_order_relaxed) ==
-                    ((static_cast<uint64_t>(fi) << 32) | static_cast<uint32_t>(k - iptr[v])))
-              ++c;
-          }
-          off[fi + 1] = c;
-        }
-      }, 4096);
-      for (long fi = 0; fi < nf; ++fi) off[fi + 1] += off[fi];
-      parallel_for(nf, [&](long b, long e) {  // pass 3: append in (f, k) order
-        for (long fi = b; fi < e; ++fi) {
-          const int v = queue[lo + fi];
-          long pos = next + off[fi];
-          for (int k = iptr[v]; k < iptr[v + 1]; ++k) {
-            const int u = inbr[k];
-            if (perm[u] < 0 &&
-                best[u].load(std::memory_order_relaxed) ==
-                    ((static_cast<uint64_t>(fi) << 32) | static_cast<uint32_t>(k - iptr[v])))
-              queue[pos++] = u;
-          }
-        }
-      }, 4096);
-      // perm of the new vertices after pass 3 (passes 2 and 3 test perm < 0)
-      const long added = off[nf];
-      parallel_for(added, [&](long b, long e) {
-        for (long i = b; i < e; ++i) perm[queue[next + i]] = static_cast<int>(next + i);
-      });
-      next += static_cast<int>(added);
-      lo = hi;
-    }
-  }
-  if (const char* c = std::getenv("PFE_BFS_CHECK"); c && c[0] == '1') {
-    if (perm != bfs_storage_order_serial(n, iptr, inbr))
-      throw Error(PFE_CUDA_ERROR, "bfs_storage_order: parallel order differs from the sequential one");
-  }
-  return perm;
-}
 
 // Incidence lists in increasing edge index (the row order of M^T).
 struct Incidence {

@@ -46,24 +46,3 @@ def test_range_partition_stats_match_restatement(parts):
         assert st["sends"][r] == len(snd)
     assert st["owned"].sum() == g.n
 
-
-def test_parallel_bfs_order_equals_sequential(monkeypatch):
-    """The storage order of general graphs (bfs_storage_order) runs its large
-    breadth-first levels in parallel; with PFE_BFS_CHECK=1 the library also
-    runs the sequential queue and raises if the orders differ.  Random graphs
-    whose middle levels are far above the parallel threshold (2^18 incidence
-    entries), with isolated vertices as extra components."""
-    monkeypatch.setenv("PFE_BFS_CHECK", "1")
-    rng = np.random.Generator(np.random.PCG64(11))
-    for n, deg in [(300_000, 8), (120_000, 24)]:
-        a = rng.integers(0, n, size=n * deg // 2)
-        b = rng.integers(0, n, size=n * deg // 2)
-        i, j = np.minimum(a, b), np.maximum(a, b)
-        keep = i < j
-        key = np.unique(i[keep].astype(np.int64) * n + j[keep])
-        ei, ej = (key // n).astype(np.int32), (key % n).astype(np.int32)
-        w = np.ones(ei.size)
-        deg_v = np.bincount(ei, minlength=n) + np.bincount(ej, minlength=n) + 1.0
-        g = api.WeightedGraph(n, ei, ej, w, deg_v.astype(np.float64))
-        st = api.range_partition_stats(g, 4)
-        assert int(st["owned"].sum()) == n
