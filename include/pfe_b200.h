@@ -140,6 +140,12 @@ const char* pfe_last_error(void);
 pfe_params pfe_params_default(void);
 pfe_exec pfe_exec_default(void);
 int pfe_device_check(int32_t device); /* 0 if an sm_100-class device is usable */
+/* Destroyed solvers and states park their large device arrays in a per-device
+ * cache (exact-size reuse by the next solver: the one-call pfe_solve otherwise
+ * spends 0.1-1.4 s per call re-carving 24 GB for C4).  This returns the cached
+ * blocks of `device` to the driver; the result is the number of bytes released.
+ * Environment PFE_CACHE_MB caps the cache (default 40 % of device memory, 0 = off). */
+int64_t pfe_release_cached_memory(int32_t device);
 
 /* PfeSolver::PfeSolver (solver.hpp:53, solver.cpp:43-58): builds the
  * operator A = (lambda/2) M^T M + (r/2) D, its Jacobi preconditioner and the

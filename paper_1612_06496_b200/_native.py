@@ -61,6 +61,7 @@ _I = C.POINTER(C.c_int32)
 
 _SIGS = {
     "pfe_last_error": (C.c_char_p, []),
+    "pfe_release_cached_memory": (C.c_int64, [C.c_int32]),
     "pfe_params_default": (pfe_params, []),
     "pfe_exec_default": (pfe_exec, []),
     "pfe_device_check": (C.c_int, [C.c_int32]),

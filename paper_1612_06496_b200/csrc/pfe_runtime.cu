@@ -18,6 +18,7 @@
 #include <condition_variable>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -369,8 +370,90 @@ struct UninitAlloc : std::allocator<T> {
 template <class T>
 using uvec = std::vector<T, UninitAlloc<T>>;
 
+// Exact-size cache of large device blocks in front of cudaMallocAsync.  The
+// one-call C ABI (pfe_solve) builds and destroys a solver and a state per
+// call; for C4 that is 13 state arrays of 1-4.3 GB.  The driver's pool does
+// keep freed memory, but re-carving it for the next call cost 140-1400 ms per
+// call (measured under bench.py, gpurun_out/bench_e2e_c4.err), several times
+// the copies themselves.  Blocks >= kMin bytes released at destruction --
+// when nothing is pending on them: every entry point synchronises its stream
+// before it returns -- are parked here per device and handed back to the next
+// allocation of exactly that size.  The cache holds at most `cap` bytes per
+// device (PFE_CACHE_MB, default 40 % of device memory; 0 disables it); on an
+// allocation failure it is flushed and the allocation retried.
+struct BlockCache {
+  static constexpr size_t kMin = 8u << 20;
+  struct PerDev {
+    std::multimap<size_t, void*> blocks;
+    size_t bytes = 0;
+    size_t cap = 0;
+    bool cap_set = false;
+  };
+  std::mutex mu;
+  PerDev dev[64];
+  static int current() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d >= 0 && d < 64 ? d : 0;
+  }
+  void set_cap(PerDev& pd) {
+    if (pd.cap_set) return;
+    pd.cap_set = true;
+    if (const char* e = std::getenv("PFE_CACHE_MB")) {
+      pd.cap = static_cast<size_t>(std::strtoull(e, nullptr, 10)) << 20;
+      return;
+    }
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      tot = 0;
+    }
+    pd.cap = tot / 5 * 2;
+  }
+  void* take(size_t bytes) {
+    if (bytes < kMin) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    PerDev& pd = dev[current()];
+    auto it = pd.blocks.find(bytes);
+    if (it == pd.blocks.end()) return nullptr;
+    void* p = it->second;
+    pd.blocks.erase(it);
+    pd.bytes -= bytes;
+    return p;
+  }
+  bool park(void* p, size_t bytes) {
+    if (bytes < kMin) return false;
+    std::lock_guard<std::mutex> lk(mu);
+    PerDev& pd = dev[current()];
+    set_cap(pd);
+    if (pd.bytes + bytes > pd.cap) return false;
+    pd.blocks.emplace(bytes, p);
+    pd.bytes += bytes;
+    return true;
+  }
+  // returns the cached bytes it gave back to the driver's pool
+  size_t flush() {
+    std::lock_guard<std::mutex> lk(mu);
+    PerDev& pd = dev[current()];
+    const size_t was = pd.bytes;
+    for (auto& kv : pd.blocks) cudaFreeAsync(kv.second, nullptr);
+    pd.blocks.clear();
+    pd.bytes = 0;
+    if (was) cudaStreamSynchronize(nullptr);
+    return was;
+  }
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();  // never destroyed: no CUDA calls at exit
+  return *c;
+}
+
 struct DevPool {
-  std::vector<void*> ptrs;
+  struct Block {
+    void* p;
+    size_t bytes;
+  };
+  std::vector<Block> ptrs;
   cudaStream_t stream = nullptr;   // allocation stream, set before the first allocation
   cudaStream_t fstream = nullptr;  // free stream: a state may outlive its solver's
                                    // stream, so states free on the legacy stream (every
@@ -378,9 +461,17 @@ struct DevPool {
   template <class T>
   T* alloc(size_t count) {
     if (count == 0) count = 1;
-    void* p = nullptr;
-    CK(cudaMallocAsync(&p, count * sizeof(T), stream));
-    ptrs.push_back(p);
+    const size_t bytes = count * sizeof(T);
+    void* p = block_cache().take(bytes);
+    if (!p) {
+      cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+      if (e == cudaErrorMemoryAllocation && block_cache().flush() > 0) {
+        cudaGetLastError();
+        e = cudaMallocAsync(&p, bytes, stream);
+      }
+      CK(e);
+    }
+    ptrs.push_back({p, bytes});
     return static_cast<T*>(p);
   }
   template <class T, class A>
@@ -389,15 +480,18 @@ struct DevPool {
     if (!v.empty()) copy_h2d(d, v.data(), v.size() * sizeof(T), s);
     return d;
   }
+  // mid-lifetime release: stream-ordered (work on the block may be pending)
   void release(void* p) {
-    auto it = std::find(ptrs.begin(), ptrs.end(), p);
+    auto it = std::find_if(ptrs.begin(), ptrs.end(), [p](const Block& b) { return b.p == p; });
     if (it != ptrs.end()) {
       cudaFreeAsync(p, fstream);
       ptrs.erase(it);
     }
   }
+  // at destruction: nothing is pending on the blocks (see BlockCache)
   void free_all() {
-    for (void* p : ptrs) cudaFreeAsync(p, fstream);
+    for (const Block& b : ptrs)
+      if (!block_cache().park(b.p, b.bytes)) cudaFreeAsync(b.p, fstream);
     ptrs.clear();
   }
   ~DevPool() { free_all(); }
@@ -2153,6 +2247,16 @@ void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, v
 extern "C" {
 
 const char* pfe_last_error(void) { return g_last_error.c_str(); }
+
+int64_t pfe_release_cached_memory(int32_t device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return 0;
+  }
+  DeviceGuard g(device);
+  return static_cast<int64_t>(block_cache().flush());
+}
 
 pfe_params pfe_params_default(void) {
   pfe_params p{};

@@ -70,3 +70,27 @@ def test_nonconverged_columns_warn_on_stderr(kw, capfd):
     lines = [ln for ln in err.splitlines() if ln.startswith("pfe: inner solve column")]
     assert len(lines) == 2 * prm.dim, err  # 2 inner iterations x d columns
     assert "stopped at rel residual" in lines[0]
+
+
+@pytest.mark.gpu
+def test_block_cache_reuses_and_releases_device_memory():
+    """Destroyed solvers park their large device arrays for exact-size reuse
+    (the one-call pfe_solve path); pfe_release_cached_memory hands them back."""
+    from paper_1612_06496_b200 import _native as N
+
+    lib = N.load()
+    lib.pfe_release_cached_memory(0)
+    rng = np.random.Generator(np.random.PCG64(3))
+    img, _ = voronoi_image(512, 640, 6, 0.05, rng)  # n*d*8 = 10.5 MB per state array: above the 8 MB cache floor
+    g = grid_graph(img, 0.1, 1)
+    prm = api.PfeParams(dim=4, lambda_=1.0, r=1.0, soc_max=1, sb_max_stage1=2, sb_max_stage2=0, conv_tol=0.0,
+                        pcg=api.PcgConfig(1e-6, 50, api.Preconditioner.Jacobi))
+    y0 = api.random_embedding(g.n, 4, 0, g.degree)
+    ya = api.soc(g, prm, y0)
+    yb = api.soc(g, prm, y0)  # runs on recycled (uncleared) blocks: must not depend on their contents
+    assert np.array_equal(ya, yb)
+    freed = lib.pfe_release_cached_memory(0)
+    assert freed >= 10 * g.n * 4 * 8
+    assert lib.pfe_release_cached_memory(0) == 0
+    assert np.array_equal(api.soc(g, prm, y0), ya)
+    assert lib.pfe_release_cached_memory(99) == 0
