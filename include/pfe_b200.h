@@ -39,7 +39,9 @@ extern "C" {
  * set-up) applied by level-scheduled device triangular solves, host-driven
  * PCG loop on the general-graph kernels.  A factor that breaks down after
  * every shift runs Jacobi and reports jacobi_fallback = 1, as the reference
- * does (pcg.cpp:22-28); so do the row-band / vertex-range solvers.
+ * does (pcg.cpp:22-28).  Row-band / vertex-range (multi-GPU) solvers keep the
+ * factor of the GLOBAL matrix on every rank and apply it to the all-gathered
+ * residual, so they reproduce the single-GPU IC(0) iterates.
  * pfe_split_bregman_standalone and pfe_pcg_solve_multi
  * (PcgOperator::solve_multi) factor their matrix the same way. */
 #define PFE_PRECOND_IC0 0

@@ -549,7 +549,7 @@ def band_plan(height: int, nranks: int, radius: int, rank: int) -> Tuple[int, in
 
 
 def soc_banded(g: WeightedGraph, params: PfeParams, y0, nbands: int, two_stage: bool = False,
-               device: int = 0) -> np.ndarray:
+               device: int = 0, return_report: bool = False):
     """The multi-GPU partitioned algorithm with `nbands` parts emulated on one
     device: row bands for pixel grids (grid hint), vertex ranges with ghost
     rows for general graphs."""
@@ -559,11 +559,12 @@ def soc_banded(g: WeightedGraph, params: PfeParams, y0, nbands: int, two_stage: 
     rep = N.pfe_report()
     _check(N.load().pfe_solve_banded(C.byref(gc), C.byref(pc), C.byref(xc), int(nbands), 1 if two_stage else 0,
                                      N.dptr(y0c), N.dptr(out), C.byref(rep)))
-    return _from_colmajor(out, g.n, params.dim)
+    y = _from_colmajor(out, g.n, params.dim)
+    return (y, {k: getattr(rep, k) for k, _ in N.pfe_report._fields_}) if return_report else y
 
 
 def soc_multi_gpu(g: WeightedGraph, params: PfeParams, y0, devices, two_stage: bool = False,
-                  return_ms: bool = False):
+                  return_ms: bool = False, return_report: bool = False):
     """soc / pfe_two_stage of one graph over several GPUs from ONE call
     (pfe_solve_multi_gpu): row bands (pixel grids) or vertex ranges (general
     graphs), one band per listed device, NCCL communicators from
@@ -577,6 +578,8 @@ def soc_multi_gpu(g: WeightedGraph, params: PfeParams, y0, devices, two_stage: b
     _check(N.load().pfe_solve_multi_gpu(C.byref(gc), C.byref(pc), C.byref(xc), int(devs.size), N.iptr(devs),
                                         1 if two_stage else 0, N.dptr(y0c), N.dptr(out), C.byref(rep), N.dptr(ms)))
     y = _from_colmajor(out, g.n, params.dim)
+    if return_report:
+        return y, {k: getattr(rep, k) for k, _ in N.pfe_report._fields_}
     return (y, float(ms[0])) if return_ms else y
 
 

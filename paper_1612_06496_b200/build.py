@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -46,11 +47,31 @@ def _headers():
     return list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list(INCLUDE.glob("*.h"))
 
 
+_INC = re.compile(r'^\s*#\s*include\s*"([^"]+)"', re.M)
+
+
+def _deps(src: Path, seen: set | None = None) -> set:
+    """Project headers `src` includes, transitively (quoted includes found
+    under csrc/ or include/)."""
+    seen = set() if seen is None else seen
+    for name in _INC.findall(src.read_text(errors="ignore")):
+        for base in (src.parent, CSRC, INCLUDE):
+            h = (base / name).resolve()
+            if h.exists() and h not in seen:
+                seen.add(h)
+                _deps(h, seen)
+                break
+    return seen
+
+
 def _stale(obj: Path, src: Path, hdr_mtime: float) -> bool:
+    """A TU is rebuilt when it, or a header it includes, is newer than its object."""
     if not obj.exists():
         return True
     m = obj.stat().st_mtime
-    return m < src.stat().st_mtime or m < hdr_mtime
+    if m < src.stat().st_mtime:
+        return True
+    return any(m < h.stat().st_mtime for h in _deps(src))
 
 
 def build(verbose: bool = False, jobs: int | None = None) -> Path:

@@ -152,6 +152,44 @@ void setup_band_grid(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad
   }
 }
 
+// IC(0) for partitioned solvers (the reference default, pcg.cpp:22-28).  The
+// factor depends on the global row order, and its triangular solves are
+// sequential across any row partition, so every rank keeps the factor of the
+// GLOBAL matrix (built exactly as the single-GPU solver builds it) and
+// applies it to the gathered global residual; it then uses its own rows of
+// z.  All ranks compute the same z and the same r.z total (bitwise the
+// single-GPU values), so no rank waits on another inside a sweep.  `pos`
+// maps a vertex to its row in the team's global order (identity for row
+// bands, the breadth-first storage position for vertex ranges).
+void setup_team_ic(pfe_solver* S, const HostGraph& hg, const Incidence& inc, const std::vector<int>& pos) {
+  const int n = hg.n;
+  const double hl = 0.5 * S->prm.lambda, dterm = 0.5 * S->prm.r;
+  std::vector<double> diag(static_cast<size_t>(n));
+  parallel_for(n, [&](long vb, long ve) {
+    for (long v = vb; v < ve; ++v) {
+      double acc = 0.0;
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) acc += (hl * inc.iw[k]) * inc.iw[k];
+      diag[v] = acc + dterm * hg.deg[v];  // the (r/2) d_v triplet is summed last
+    }
+  }, 4096);
+  std::vector<int> nptr, ncol;
+  std::vector<double> nval;
+  natural_rows(n, inc, hl, diag.data(), nptr, ncol, nval);
+  const int n_local = S->n;
+  S->ic = true;
+  build_ic(S, n, nptr, ncol, nval, pos);  // clears S->ic and sets jacobi_fallback on a breakdown
+  S->ic_team = S->ic;
+  S->ic = false;  // the single-GPU IC loop is not used by teams
+  S->jacobi_fallback = !S->ic_team;
+  if (S->ic_team) {
+    S->rfull = S->mem.alloc<double>(static_cast<size_t>(n) * S->d);
+    S->ic_part = S->mem.alloc<double>(static_cast<size_t>(std::max(1, std::min(S->max_grid, (n + 255) / 256))) * S->d);
+    std::vector<double> one(static_cast<size_t>(n_local), 1.0);
+    S->ones = S->mem.upload(one, S->stream);
+    CK(cudaStreamSynchronize(S->stream));
+  }
+}
+
 pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int nranks, int rank,
                                void* comm) {
   if (!g || !p) config_error("null graph or params");
@@ -192,6 +230,11 @@ pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pf
   const size_t rows = static_cast<size_t>(S->max_own) * d;
   S->ystage = S->mem.alloc<double>(rows);
   S->yall = S->mem.alloc<double>(rows * nranks);
+  if (p->preconditioner == PFE_PRECOND_IC0) {
+    std::vector<int> ident(static_cast<size_t>(g->n));
+    std::iota(ident.begin(), ident.end(), 0);
+    setup_team_ic(S.get(), hg, build_incidence(hg), ident);
+  }
   S->ensure_log(64);
   CK(cudaStreamSynchronize(S->stream));
   S->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -331,6 +374,57 @@ int nb_producer_init(const pfe_solver* S, bool) {
   return nb_init;
 }
 
+// First row of a member's owned block in the team's global row order.
+long team_global_first(const pfe_solver* S) {
+  return S->part == 2 ? static_cast<long>(S->range_start[S->rank]) : static_cast<long>(S->band_r0) * S->band_w;
+}
+
+// Owned rows of `field` from every member -> every member's S->rfull, a
+// [global n][d] array in the team's global row order (IC(0) residual).
+template <class F>
+void team_gather_rows(Team& t, F&& field) {
+  const pfe_solver* S0 = t.S(0);
+  const int d = S0->d, P = S0->nranks;
+  if (t.emulated) {
+    team_sync(t);
+    for (size_t j = 0; j < t.size(); ++j)
+      for (size_t i = 0; i < t.size(); ++i) {
+        const pfe_solver* Si = t.S(i);
+        emu_copy(t.S(j), t.S(j)->rfull + static_cast<size_t>(team_global_first(Si)) * d,
+                 field(t.st[i]) + Si->own_vb * d, static_cast<size_t>(Si->own_cnt) * d);
+      }
+    team_sync(t);
+    return;
+  }
+  const size_t slot = static_cast<size_t>(S0->max_own) * d;
+  {
+    NcclGroup grp;
+    for (pfe_state* st : t.st) {
+      pfe_solver* S = on(st->s);
+      CK(cudaMemcpyAsync(S->ystage, field(st) + S->own_vb * d, sizeof(double) * S->own_cnt * d,
+                         cudaMemcpyDeviceToDevice, S->stream));
+      nccl_check(nccl().AllGather(S->ystage, S->yall, slot, ncclDouble, static_cast<ncclComm_t>(S->comm), S->stream),
+                 "ncclAllGather(r)");
+    }
+  }
+  for (pfe_state* st : t.st) {
+    pfe_solver* S = on(st->s);
+    for (int q = 0; q < P; ++q) {
+      long first, cnt;
+      if (S->part == 2) {
+        first = S->range_start[q];
+        cnt = S->range_start[q + 1] - S->range_start[q];
+      } else {
+        const BandPlan bp = band_plan(S->band_h, P, S->band_rad, q);
+        first = static_cast<long>(bp.r0) * S->band_w;
+        cnt = static_cast<long>(bp.r1 - bp.r0) * S->band_w;
+      }
+      CK(cudaMemcpyAsync(S->rfull + static_cast<size_t>(first) * d, S->yall + q * slot, sizeof(double) * cnt * d,
+                         cudaMemcpyDeviceToDevice, S->stream));
+    }
+  }
+}
+
 // One PCG solve of every band (pcg.cpp:40-114 for all d columns).
 //
 // The host does not read the device control block after every PCG
@@ -356,17 +450,60 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
     a[i].nb_init = a[i].nb_update = a[i].nb_spmv = S->nranks;
   }
   const int maxit = t.S(0)->prm.pcg_max_iter;
+  const bool ranges = t.S(0)->part == 2;
+  const bool ic = t.S(0)->ic_team;
+  // IC(0): z = M^-1 r on the gathered global residual, on every member; the
+  // r.z total the consumers read (slot 2 after init, slot 1 after an update)
+  // becomes the preconditioned one: member 0's entry holds the global total
+  // (k_ic_dot over the global vectors, the single-GPU value), the others 0.
+  std::vector<pfe_dev::PcgArgs> az(a);  // SpMV arguments when z replaces D^-1 r
+  std::vector<TopoDesc> tz(B);
+  for (size_t i = 0; i < B && ic; ++i) {
+    pfe_solver* S = t.S(i);
+    const long g0 = team_global_first(S) - S->own_vb;  // global row of local row 0 (row bands)
+    tz[i] = S->topo;
+    if (ranges) {
+      a[i].zbuf = S->zbuf + static_cast<size_t>(team_global_first(S)) * S->d;  // owned rows are contiguous
+    } else {
+      az[i].r = S->zbuf + static_cast<size_t>(g0) * S->d;  // band rows incl. halo are contiguous global rows
+      tz[i].g1.invd = S->ones;
+      tz[i].g2.invd = S->ones;
+    }
+  }
+  using DSeq = std::make_integer_sequence<int, pfe_dev::kMaxD>;
+  auto ic_z = [&](int slot, bool to_p0) {
+    if (!ic) return;
+    team_gather_rows(t, [](pfe_state* st) { return st->r; });
+    for (size_t i = 0; i < B; ++i) {
+      pfe_solver* S = on(t.S(i));
+      const int d = S->d, P = S->nranks;
+      const int gn = static_cast<int>(S->global_n);
+      ic_apply_dispatch(d, DSeq{}, S->icd, S->rfull, S->zbuf, S->stream);
+      const int grid = std::min(S->max_grid, std::max(1, (gn + 255) / 256));
+      // (its own partials: iterations issued after every column stopped re-read
+      // the update's block partials, which must stay as that update left them)
+      ic_dot_dispatch(d, DSeq{}, gn, S->rfull, S->zbuf, S->ic_part, S->ctl, S->gathered_a + slot * d, grid, S->stream);
+      for (int q = 1; q < P; ++q)
+        CK(cudaMemsetAsync(S->gathered_a + (static_cast<size_t>(q) * 3 + slot) * d, 0, sizeof(double) * d, S->stream));
+      if (to_p0)  // p = z for the first iteration: owned rows (halo / ghost rows are exchanged next)
+        CK(cudaMemcpyAsync(t.st[i]->pb[0] + S->own_vb * d,
+                           S->zbuf + static_cast<size_t>(team_global_first(S)) * d,
+                           sizeof(double) * S->own_cnt * d, cudaMemcpyDeviceToDevice, S->stream));
+      CK(cudaGetLastError());
+    }
+  };
   for (size_t i = 0; i < B; ++i) on(t.S(i))->tab->pcg_init(t.S(i)->topo, a[i], t.S(i)->lv());
   team_gather_totals(t, 3, false, nb_producer_init);
+  ic_z(2, true);
   team_halo(t, [](pfe_state* st) { return st->pb[0]; });
   auto spmv = [&](int k) {
     for (size_t i = 0; i < B; ++i) {
-      a[i].phase = pfe_dev::pcg_phase(k);
-      on(t.S(i))->tab->pcg_spmv(t.S(i)->topo, a[i], t.S(i)->lv());
+      a[i].phase = az[i].phase = pfe_dev::pcg_phase(k);
+      const bool zdir = ic && !ranges;
+      on(t.S(i))->tab->pcg_spmv(zdir ? tz[i] : t.S(i)->topo, zdir ? az[i] : a[i], t.S(i)->lv());
     }
     team_gather_totals(t, 1, true, nb_producer);
   };
-  const bool ranges = t.S(0)->part == 2;
   // one PCG iteration after the SpMV of iteration k: update k, SpMV k + 1
   auto iteration = [&](int k) {
     // (row bands need no halo exchange of p here: the SpMV stored the halo
@@ -376,6 +513,7 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
       on(t.S(i))->tab->pcg_update(t.S(i)->topo, a[i], t.S(i)->lv());
     }
     team_gather_totals(t, 3, false, nb_producer);
+    ic_z(1, false);
     const int kn = k + 1;
     if (ranges) {
       // vertex ranges: p' = D^-1 r + beta p on owned rows, then its ghosts
@@ -385,7 +523,7 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
         on(t.S(i))->tab->pcg_pdir(t.S(i)->topo, a[i], t.S(i)->lv());
       }
       team_halo(t, [kn](pfe_state* st) { return (kn & 1) ? st->pb[0] : st->pb[1]; });
-    } else {
+    } else if (!ic) {  // with IC(0) every band already holds z on its halo rows
       team_halo(t, [](pfe_state* st) { return st->r; });
     }
     spmv(kn);
@@ -789,6 +927,7 @@ pfe_solver* create_range_solver(const pfe_graph* g, const pfe_params* p, const p
   S->gathered_b = S->mem.alloc<double>(static_cast<size_t>(P) * d);
   S->ystage = S->mem.alloc<double>(static_cast<size_t>(S->max_own) * d);
   S->yall = S->mem.alloc<double>(static_cast<size_t>(S->max_own) * d * P);
+  if (p->preconditioner == PFE_PRECOND_IC0) setup_team_ic(S.get(), hg, inc, pos);
   S->ensure_log(64);
   CK(cudaStreamSynchronize(S->stream));
   S->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

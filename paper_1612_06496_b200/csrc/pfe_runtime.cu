@@ -675,6 +675,14 @@ struct pfe_solver {
   bool ic = false;
   IcDev icd{};
   double* zbuf = nullptr;
+  // Row-band / vertex-range solvers with IC(0): the factor of the GLOBAL
+  // matrix lives on every rank (icd), each rank applies it to the gathered
+  // global residual (rfull -> zbuf, both [global n][d] in the team's global
+  // row order) and uses its own rows of z (pfe_band.cuh: team_pcg).
+  bool ic_team = false;
+  double* rfull = nullptr;
+  double* ic_part = nullptr;  // block partials of the global r.z reduction
+  double* ones = nullptr;  // [local n] 1.0: the tiled SpMV forms 1.0 * z + beta p
   double setup_s = 0.0;
   int pred_iters = 1;
   Prof prof;
@@ -1151,6 +1159,42 @@ Incidence build_incidence(const HostGraph& g) {
   return c;
 }
 
+// A = (lambda/2) M^T M + (r/2) D in the reference's natural row order: rows
+// sorted by column, duplicate columns summed in edge order, exact zeros
+// dropped (csr_from_triplets over form_normal_matrix's triplets,
+// sparse.cpp:96-122).  `diag` holds the finished diagonal per vertex.
+void natural_rows(int n, const Incidence& inc, double hl, const double* diag, std::vector<int>& nptr,
+                  std::vector<int>& ncol, std::vector<double>& nval) {
+  nptr.assign(static_cast<size_t>(n) + 1, 0);
+  ncol.clear();
+  nval.clear();
+  ncol.reserve(inc.inbr.size() + n);
+  nval.reserve(inc.inbr.size() + n);
+  std::vector<std::pair<int, double>> row;
+  for (int v = 0; v < n; ++v) {
+    row.clear();
+    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) row.emplace_back(inc.inbr[k], -((hl * inc.iw[k]) * inc.iw[k]));
+    row.emplace_back(v, diag[v]);
+    std::stable_sort(row.begin(), row.end(),
+                     [](const std::pair<int, double>& a, const std::pair<int, double>& b) { return a.first < b.first; });
+    for (size_t t = 0; t < row.size();) {
+      const int col = row[t].first;
+      double s = 0.0;
+      if (col == v) {
+        s = row[t].second;
+        ++t;
+      } else {
+        for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
+      }
+      if (s != 0.0) {
+        ncol.push_back(col);
+        nval.push_back(s);
+      }
+    }
+    nptr[v + 1] = static_cast<int>(ncol.size());
+  }
+}
+
 // Builds the device topology.  Diagonal of A: sum over incident edges in
 // edge order of (hl * w) * w, then + (0.5 r) deg_v last — the accumulation
 // order csr_from_triplets applies to form_normal_matrix's triplets.
@@ -1537,35 +1581,11 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
       std::copy(tval.begin() + ub[x], tval.begin() + ub[x] + tlen[x], aval.begin() + aptr[x]);
     }
   }, 4096);
-  std::vector<std::pair<int, double>> row;
   if (S->ic) {
     // A in the reference's row order (the IC(0) factor depends on it)
-    std::vector<int> nptr(static_cast<size_t>(n) + 1, 0), ncol;
+    std::vector<int> nptr, ncol;
     std::vector<double> nval;
-    ncol.reserve(acol.size());
-    nval.reserve(aval.size());
-    for (int v = 0; v < n; ++v) {
-      row.clear();
-      for (int k = iptr[v]; k < iptr[v + 1]; ++k) row.emplace_back(inbr[k], -((hl * iw[k]) * iw[k]));
-      row.emplace_back(v, diag[v]);
-      std::stable_sort(row.begin(), row.end(),
-                       [](const std::pair<int, double>& a, const std::pair<int, double>& b) { return a.first < b.first; });
-      for (size_t t = 0; t < row.size();) {
-        const int col = row[t].first;
-        double s = 0.0;
-        if (col == v) {
-          s = row[t].second;
-          ++t;
-        } else {
-          for (; t < row.size() && row[t].first == col; ++t) s += row[t].second;
-        }
-        if (s != 0.0) {
-          ncol.push_back(col);
-          nval.push_back(s);
-        }
-      }
-      nptr[v + 1] = static_cast<int>(ncol.size());
-    }
+    natural_rows(n, inc, hl, diag.data(), nptr, ncol, nval);
     build_ic(S, n, nptr, ncol, nval, perm);
   }
   // edge storage follows the vertex storage order: the edges a vertex owns

@@ -143,3 +143,59 @@ def test_multi_gpu_rejects_repeated_devices():
     y0 = api.random_embedding(g.n, 2, 1, g.degree)
     with pytest.raises(api.ConfigError, match="distinct"):
         api.soc_multi_gpu(g, prm, y0, [0, 0])
+
+
+# ------------------------------------------------ IC(0) on partitioned solvers --
+def ic_params(d, soc=2, sb=3, stage2=0):
+    return api.PfeParams(dim=d, lambda_=100.0, r=1.0, soc_max=soc, sb_max_stage1=sb, sb_max_stage2=stage2,
+                         conv_tol=0.0, pcg=api.PcgConfig(1e-6, 200, api.Preconditioner.Ic0))
+
+
+@pytest.mark.parametrize("radius,d,nbands", [(1, 4, 2), (1, 3, 3), (2, 8, 2)])
+def test_bands_ic0_match_single_gpu_ic0(radius, d, nbands):
+    """The reference's default preconditioner on row bands: every band applies
+    the factor of the GLOBAL matrix to the gathered residual (pfe_band.cuh
+    setup_team_ic), so the bands reproduce the single-GPU IC(0) solve and the
+    oracle's, with no Jacobi fallback."""
+    g = image_graph(31, 44, 3 + nbands, radius)
+    prm = ic_params(d)
+    y0 = api.random_embedding(g.n, d, 5, g.degree)
+    single = api.soc(g, prm, y0)
+    banded, rep = api.soc_banded(g, prm, y0, nbands, return_report=True)
+    assert rep["jacobi_fallback"] == 0
+    err = rel(banded, single)
+    erro = rel(banded, O.solve(g, prm, y0, mode=0))
+    print(f"IC(0) bands R={radius} d={d} P={nbands}: vs single GPU {err:.3e}, vs oracle {erro:.3e}")
+    assert err <= 1e-10
+    assert erro <= 1e-9
+    # the Jacobi path on the same bands gives a different iterate history: the
+    # preconditioner is really applied
+    jac = api.PfeParams(dim=d, lambda_=100.0, r=1.0, soc_max=2, sb_max_stage1=3, sb_max_stage2=0, conv_tol=0.0,
+                        pcg=api.PcgConfig(1e-6, 5, api.Preconditioner.Jacobi))
+    assert rel(api.soc_banded(g, jac, y0, nbands), single) > 1e-8
+
+
+@pytest.mark.parametrize("nparts,d", [(2, 3), (3, 4)])
+def test_vertex_ranges_ic0_match_single_gpu_ic0(nparts, d):
+    g = knn_points_graph(700, 8, 30 + nparts)
+    prm = ic_params(d, stage2=3)
+    y0 = api.random_embedding(g.n, d, 6, g.degree)
+    single = api.pfe_two_stage(g, prm, y0)
+    ranged, rep = api.soc_banded(g, prm, y0, nparts, two_stage=True, return_report=True)
+    assert rep["jacobi_fallback"] == 0
+    err = rel(ranged, single)
+    print(f"IC(0) ranges d={d} P={nparts}: vs single GPU {err:.3e}")
+    assert err <= 1e-10
+    assert rel(ranged, O.solve(g, prm, y0, mode=1)) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", ["grid8", "knn"])
+def test_multi_gpu_one_call_ic0(kind):
+    """IC(0) through pfe_solve_multi_gpu (NCCL all-gather of the residual on
+    the visible GPUs)."""
+    g = knn_points_graph(500, 8, 9) if kind == "knn" else image_graph(29, 36, 6, 1)
+    prm = ic_params(3)
+    y0 = api.random_embedding(g.n, 3, 2, g.degree)
+    y, rep = api.soc_multi_gpu(g, prm, y0, list(range(gpu_count())), return_report=True)
+    assert rep["jacobi_fallback"] == 0
+    assert rel(y, api.soc(g, prm, y0)) <= 1e-10
