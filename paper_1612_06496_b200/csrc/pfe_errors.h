@@ -36,4 +36,31 @@ long grid_graph_device(int H, int W, const double* rgb, double sigma_rgb, int ra
 long knn_graph_from_lists(int n, int k, const double* d2, const int32_t* idx, int32_t* ei, int32_t* ej, double* w,
                           double* degree, double* sigma_out);
 
+// General-graph solver topology built on the device (pfe_csrbuild.cu): all
+// pointers are device arrays in storage order, allocated through `alloc`.
+struct CsrDevArrays {
+  int* aptr = nullptr;   // [n + 1] rows of A
+  int* acol = nullptr;   // [nnz] storage rows, reference column order
+  double* aval = nullptr;
+  int* iptr = nullptr;   // [n + 1] incidence lists, increasing edge index
+  int* inbr = nullptr;   // [2m] neighbour storage row
+  int* ieid = nullptr;   // [2m] edge row << 1 | [vertex is the edge's first endpoint]
+  double* iw = nullptr;  // [2m]
+  double* diag = nullptr;
+  double* invd = nullptr;
+  double* deg = nullptr;
+  double* sqd = nullptr;
+  int* perm = nullptr;          // [n] vertex -> storage row
+  int32_t* edge_row = nullptr;  // [m] edge -> row of the edge arrays
+  long nnz = 0;
+  int components = 0;
+};
+using DevAllocFn = void* (*)(void* ctx, size_t bytes);
+using H2dFn = void (*)(void* dst, const void* src, size_t bytes, void* stream);
+// false: more than max_components connected components (the level-synchronous
+// device BFS would crawl; the caller builds on the host instead).
+bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, const double* w, const double* degree,
+                         double hl, double dterm, bool precond_none, void* stream, DevAllocFn alloc, void* alloc_ctx,
+                         H2dFn h2d, int max_components, CsrDevArrays* out);
+
 }  // namespace pfe_host

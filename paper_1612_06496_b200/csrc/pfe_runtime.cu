@@ -1489,6 +1489,50 @@ void build_topology(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad)
     return;
   }
 
+  // General graph on the device (pfe_csrbuild.cu): every array derived from
+  // the uploaded edge list by kernels, bit-identical to the host builder
+  // below.  IC(0) solvers need A on the host (the factor), and graphs with
+  // very many components fall through to the host builder.
+  {
+    const char* sw = std::getenv("PFE_DEVICE_CSR");
+    const bool host_only = std::getenv("PFE_HOST_TOPOLOGY") && std::getenv("PFE_HOST_TOPOLOGY")[0] == '1';
+    const bool want = sw ? sw[0] == '1' : m >= (1L << 17);
+    if (want && !host_only && !S->ic && !(sw && sw[0] == '0')) {
+      pfe_host::CsrDevArrays o;
+      auto alloc = [](void* ctx, size_t bytes) -> void* {
+        return static_cast<pfe_solver*>(ctx)->mem.alloc<char>(bytes);
+      };
+      auto h2d = [](void* dst, const void* src, size_t bytes, void* stream) {
+        copy_h2d(dst, src, bytes, static_cast<cudaStream_t>(stream));
+      };
+      if (pfe_host::csr_topology_device(n, m, g.ei, g.ej, g.w, g.deg, hl, dterm,
+                                        S->prm.preconditioner == PFE_PRECOND_NONE, st, alloc, S, h2d, 4096, &o)) {
+        S->diag = o.diag;
+        S->invd = o.invd;
+        S->deg = o.deg;
+        S->sqd = o.sqd;
+        S->perm_d = o.perm;
+        S->d_edge_slot = o.edge_row;  // the host copy is downloaded on first use (state get / set)
+        S->edge_rows = m;
+        pfe_dev::Csr c{};
+        c.n = n;
+        c.vb = 0;
+        c.ve = n;
+        c.aptr = o.aptr;
+        c.acol = o.acol;
+        c.aval = o.aval;
+        c.iptr = o.iptr;
+        c.inbr = o.inbr;
+        c.ieid = o.ieid;
+        c.iw = o.iw;
+        c.invd = S->invd;
+        S->topo.kind = pfe_host::kTopoCsr;
+        S->topo.csr = c;
+        return;
+      }
+    }
+  }
+
   // incidence lists in increasing edge index (the row order of M^T)
   const bool tmr = [] {
     const char* e = std::getenv("PFE_SETUP_TIMING");
@@ -2174,6 +2218,7 @@ void warn_from_log(pfe_solver* S, long lo, long hi) {
 }
 
 enum CallKind { kCallSplit = 0, kCallSoc = 1, kCallTwoStage = 2 };
+constexpr int kPieceOuter = 3;  // graph piece: one outer iteration (split_bregman + projection)
 
 // Executes a call either host-driven or as one cached CUDA graph.
 void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* user);
@@ -2216,45 +2261,78 @@ void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, v
     check_flags(S);
     return;
   }
-  // graph key: call shape + the state bookkeeping the capture bakes in
-  const auto key = std::make_tuple(kind, a0, a1, st->y == st->ybuf[0] ? 0 : 1, st->eb_cur, st->inner_zero ? 1 : 0,
-                                   st->rq_valid ? 1 : 0);
-  auto it = st->graphs.execs.find(key);
-  if (it == st->graphs.execs.end()) {
-    const Book pre{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
-    const long inner0 = S->inner_launched;
-    cudaGraph_t graph;
-    CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeRelaxed));
-    try {
-      body(RunMode{true, nullptr, nullptr});
-    } catch (...) {
-      cudaStreamEndCapture(S->stream, &graph);
-      throw;
-    }
-    CK(cudaStreamEndCapture(S->stream, &graph));
-    GraphEntry ge{};
-    CK(cudaGraphInstantiate(&ge.exec, graph, 0));
-    CK(cudaGraphDestroy(graph));
-    ge.post = Book{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
-    ge.inner = S->inner_launched - inner0;
-    st->y = pre.y;
-    st->y2 = pre.y2;
-    st->eb_cur = pre.eb_cur;
-    st->inner_zero = pre.inner_zero;
-    st->rq_valid = pre.rq_valid;
-    S->inner_launched = inner0;
-    it = st->graphs.execs.emplace(key, ge).first;
-  }
+  // One cached CUDA graph per (piece, state bookkeeping the capture bakes in).
+  // A soc / two_stage call is issued as one graph launch per outer iteration
+  // (split_bregman + projection) instead of one graph of the whole call: the
+  // graph is soc_max times smaller, which is what a one-call pfe_solve pays to
+  // capture, instantiate and destroy (C1: ~15 + 11 ms of a 51 ms call before).
+  // With an even sb_max every outer iteration finds the state bookkeeping it
+  // started from and relaunches the same executable graph; otherwise two
+  // graphs alternate.  The launches are queued back to back; the host waits
+  // once, at the end of the call.
   const long first = S->inner_launched;
-  CK(cudaGraphLaunch(it->second.exec, S->stream));
+  auto run_graph = [&](int piece, int g0, auto&& piece_body) {
+    const auto key = std::make_tuple(piece, g0, 0, st->y == st->ybuf[0] ? 0 : 1, st->eb_cur, st->inner_zero ? 1 : 0,
+                                     st->rq_valid ? 1 : 0);
+    auto it = st->graphs.execs.find(key);
+    if (it == st->graphs.execs.end()) {
+      const Book pre{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
+      const long inner0 = S->inner_launched;
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeRelaxed));
+      try {
+        piece_body(RunMode{true, nullptr, nullptr});
+      } catch (...) {
+        cudaStreamEndCapture(S->stream, &graph);
+        throw;
+      }
+      CK(cudaStreamEndCapture(S->stream, &graph));
+      GraphEntry ge{};
+      CK(cudaGraphInstantiate(&ge.exec, graph, 0));
+      CK(cudaGraphDestroy(graph));
+      ge.post = Book{st->y, st->y2, st->eb_cur, st->inner_zero, st->rq_valid};
+      ge.inner = S->inner_launched - inner0;
+      st->y = pre.y;
+      st->y2 = pre.y2;
+      st->eb_cur = pre.eb_cur;
+      st->inner_zero = pre.inner_zero;
+      st->rq_valid = pre.rq_valid;
+      S->inner_launched = inner0;
+      it = st->graphs.execs.emplace(key, ge).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, S->stream));
+    const GraphEntry& ge = it->second;
+    st->y = ge.post.y;
+    st->y2 = ge.post.y2;
+    st->eb_cur = ge.post.eb_cur;
+    st->inner_zero = ge.post.inner_zero;
+    st->rq_valid = ge.post.rq_valid;
+    S->inner_launched += ge.inner;
+  };
+  auto outer_steps = [&](int soc_max, int sb_max) {  // run_soc (solver.cpp:110-126), fixed counts
+    if (!st->rq_valid) {  // outside the graph, so the first outer iteration shares the others' graph
+      S->tab->rhs_quad(S->n, S->sqd, st->p, st->breg, st->rq, 0.5 * S->prm.r, S->le());
+      st->rq_valid = true;
+    }
+    for (int k = 0; k < soc_max; ++k) {
+      st->inner_zero = true;
+      run_graph(kPieceOuter, sb_max, [&](const RunMode& mode) {
+        split_bregman_run(st, sb_max, mode);
+        project_step(st);
+      });
+    }
+  };
+  if (kind == kCallSplit) {
+    run_graph(kCallSplit, a0, [&](const RunMode& mode) { split_bregman_run(st, a0, mode); });
+  } else if (kind == kCallSoc) {
+    outer_steps(a0, a1);
+  } else {
+    outer_steps(S->prm.soc_max, S->prm.sb_max_stage1);
+    if (S->prm.sb_max_stage2 > 0)
+      run_graph(kCallSplit, S->prm.sb_max_stage2,
+                [&](const RunMode& mode) { split_bregman_run(st, S->prm.sb_max_stage2, mode); });
+  }
   CK(cudaStreamSynchronize(S->stream));
-  const GraphEntry& ge = it->second;
-  st->y = ge.post.y;
-  st->y2 = ge.post.y2;
-  st->eb_cur = ge.post.eb_cur;
-  st->inner_zero = ge.post.inner_zero;
-  st->rq_valid = ge.post.rq_valid;
-  S->inner_launched += ge.inner;
   if (S->warn) warn_from_log(S, first, S->inner_launched);
   check_flags(S);
 }
