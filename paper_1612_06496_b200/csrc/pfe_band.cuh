@@ -589,6 +589,7 @@ void team_split_bregman(Team& t, int max_iter) {
       sa.hl = 0.5 * S->prm.lambda;
       sa.gamma = 1.0 / S->prm.lambda;
       sa.ctl = S->ctl;
+      sa.prefetch = sb_prefetch();
       S->tab->sb_pass(S->topo, sa, S->lv());
       st->eb_cur ^= 1;
       st->inner_zero = false;

@@ -537,6 +537,7 @@ struct SbArgs {
   double hl;            // lambda / 2
   double gamma;         // 1 / lambda
   Ctl* ctl;
+  int prefetch;         // general graphs: L2-prefetch a vertex's b_old rows ahead of its edge loop
 };
 
 // Per vertex v and column group: for every incident edge e (ascending edge
@@ -557,6 +558,21 @@ __global__ void __launch_bounds__(kBlock, D == 16 ? 2 : 3) k_sb_pass(Topo topo, 
     const Row<V> yv = ldg_row<V>(a.y + static_cast<long>(v) * D + c0);
 #pragma unroll
     for (int k = 0; k < V; ++k) bad |= !isfinite(yv.a[k]);
+    if constexpr (!Topo::kGrid) {
+      // The b_old rows of a vertex's edges are the pass's DRAM reads (its own
+      // rows stream, the rows owned by neighbours are scattered): ask L2 for
+      // all of them now, one request per row, split over the vertex's lanes,
+      // so the batches below find them in L2 or on their way instead of each
+      // batch paying a DRAM round trip with its registers pinned.
+      if (a.prefetch && a.b_old) {
+        const int kb = __ldg(topo.iptr + v), ke = __ldg(topo.iptr + v + 1);
+        for (int k = kb + static_cast<int>(e - static_cast<long>(v) * TPV); k < ke; k += TPV) {
+          const double* row = a.b_old + static_cast<long>(__ldg(topo.ieid + k) >> 1) * D;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+          if constexpr ((D * 8) % 128 != 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + D - 1));
+        }
+      }
+    }
     double acc[V] = {};
     struct YB {
       Row<V> y, b;

@@ -2060,6 +2060,18 @@ void solve_step(pfe_state* st, const double* rhs, const RunMode& mode) {
     pcg_solve_host(st, rhs);
 }
 
+// General-graph split-Bregman pass: L2 prefetch of the b_old rows, opt-in
+// (PFE_SB_PREFETCH=1).  Measured slower on C5 (1506 -> 1595 us per pass): the
+// pass is bound by DRAM throughput on scattered 128-byte rows, not by the
+// latency of its gathers, and the prefetches only add L2 requests.
+int sb_prefetch() {
+  static const int on = [] {
+    const char* e = std::getenv("PFE_SB_PREFETCH");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return on;
+}
+
 // PfeSolver::split_bregman (solver.cpp:73-108).
 void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
   pfe_solver* S = st->s;
@@ -2160,6 +2172,7 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
     sa.hl = hl;
     sa.gamma = gamma;
     sa.ctl = S->ctl;
+    sa.prefetch = sb_prefetch();
     S->prof.begin(4, S->stream);
     S->tab->sb_pass(S->topo, sa, S->lv());
     S->prof.end(S->stream);
