@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -315,6 +316,8 @@ struct Impl {
       cudaFuncSetAttribute(k_sb_persistent<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int nb = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sb_persistent<D, R>, TileGeo<R, D>::NT, smem);
+      if (const char* e = std::getenv("PFE_SETUP_TIMING"); e && e[0] == '1')
+        std::fprintf(stderr, "k_sb_persistent<%d,%d>: %zu B dynamic shared memory, %d block(s) per SM\n", D, R, smem, nb);
       return nb;
     }));
     if (per_sm < 1) throw std::runtime_error("persistent split-Bregman kernel does not fit on an SM");
