@@ -1001,9 +1001,22 @@ void validate(const HostGraph& g, const pfe_params& p, bool check_solver_caps) {
   if (!g.deg) config_error("form_normal_matrix: degree size mismatch");
   if (p.lambda < 0.0) config_error("form_normal_matrix: lambda must be >= 0");
   if (p.r <= 0.0) config_error("form_normal_matrix: r must be > 0");
-  for (int v = 0; v < g.n; ++v)
-    if (!(g.deg[v] > 0.0))
-      config_error("form_normal_matrix: nonpositive degree at vertex " + std::to_string(v) + " (isolated vertex)");
+  {
+    // first offending vertex, found in parallel (16.8 M vertices on C4)
+    std::atomic<long> bad_deg{g.n};
+    parallel_for(g.n, [&](long b, long e) {
+      for (long v = b; v < e; ++v)
+        if (!(g.deg[v] > 0.0)) {
+          long cur = bad_deg.load();
+          while (v < cur && !bad_deg.compare_exchange_weak(cur, v)) {
+          }
+          return;
+        }
+    });
+    if (bad_deg.load() < g.n)
+      config_error("form_normal_matrix: nonpositive degree at vertex " + std::to_string(bad_deg.load()) +
+                   " (isolated vertex)");
+  }
   if (p.pcg_rel_tol <= 0.0) config_error("PcgOperator: rel_tol must be > 0");
   if (p.pcg_max_iter < 1) config_error("PcgOperator: max_iter must be >= 1");
   if (p.dim < 1) config_error("PfeSolver: dim must be >= 1");
