@@ -490,6 +490,14 @@ struct DevPool {
   }
   // at destruction: nothing is pending on the blocks (see BlockCache)
   void free_all() {
+    // parked blocks go to the next owner on any stream: make sure the device
+    // is done with them (idle in the normal case; an exception unwinding a
+    // call may leave work queued)
+    for (const Block& b : ptrs)
+      if (b.bytes >= BlockCache::kMin) {
+        cudaDeviceSynchronize();
+        break;
+      }
     for (const Block& b : ptrs)
       if (!block_cache().park(b.p, b.bytes)) cudaFreeAsync(b.p, fstream);
     ptrs.clear();
@@ -690,6 +698,11 @@ struct pfe_solver {
   double last_ms = 0.0;  // device time of the last split_bregman / run_soc / two_stage call
 
   ~pfe_solver() {
+    // Large blocks are parked in the block cache for the next solver (any
+    // stream): nothing may be pending on them.  Normal calls have already
+    // synchronised; an exception thrown mid set-up may leave copies queued.
+    if (stream) cudaStreamSynchronize(stream);
+    if (aux) cudaStreamSynchronize(aux);
     mem.free_all();  // stream-ordered frees need the stream
     if (comm && g_comm_destroy) g_comm_destroy(comm);
     if (ev0) cudaEventDestroy(ev0);
