@@ -349,7 +349,7 @@ bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, co
   int* cand2 = tmp.get<int>(n);
   CKB(cudaMemsetAsync(pos, 0xff, sizeof(int) * n, st));
   CKB(cudaMemsetAsync(key, 0xff, sizeof(ull) * n, st));
-  int placed = 0, start = 0, comps = 0;
+  int placed = 0, start = 0, comps = 0, levels = 0;
   int* seed = d_scalar;
   int* ncand = d_scalar + 1;
   while (placed < n) {
@@ -363,6 +363,9 @@ bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, co
     int f0 = placed, f1 = placed + 1;
     placed = f1;
     for (;;) {
+      // every level costs a host round trip: chain-like graphs (thousands of
+      // levels) are left to the host builder as well
+      if (++levels > 4 * max_components) return false;
       CKB(cudaMemsetAsync(ncand, 0, sizeof(int), st));
       k_expand<<<blocks_for(f1 - f0), kT, 0, st>>>(f0, f1, jbits, order, iptr, inbr, pos, key, cand, ncand);
       int nc = 0;

@@ -57,8 +57,9 @@ struct CsrDevArrays {
 };
 using DevAllocFn = void* (*)(void* ctx, size_t bytes);
 using H2dFn = void (*)(void* dst, const void* src, size_t bytes, void* stream);
-// false: more than max_components connected components (the level-synchronous
-// device BFS would crawl; the caller builds on the host instead).
+// false: more than max_components connected components or 4 * max_components
+// breadth-first levels (the level-synchronous device BFS would crawl; the
+// caller builds on the host instead).
 bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, const double* w, const double* degree,
                          double hl, double dterm, bool precond_none, void* stream, DevAllocFn alloc, void* alloc_ctx,
                          H2dFn h2d, int max_components, CsrDevArrays* out);

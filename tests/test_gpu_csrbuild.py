@@ -110,3 +110,28 @@ def test_many_components_fall_back_to_host_builder():
     y0 = api.random_embedding(g.n, 2, 3, g.degree)
     dev, host = run(g, prm, y0, True), run(g, prm, y0, False)
     same(dev, host)
+
+
+def test_chain_like_graph_falls_back_to_host_builder():
+    """A path graph has n breadth-first levels: the level-synchronous device
+    search gives up after 16384 levels and the host builder takes over (the
+    default builder choice: m >= 2^17 edges selects the device path)."""
+    n = (1 << 17) + 50
+    ei = np.arange(0, n - 1, dtype=np.int32)
+    ej = ei + 1
+    w = np.full(ei.size, 0.7)
+    deg = np.full(n, 1.4)
+    deg[0] = deg[-1] = 0.7
+    g = api.WeightedGraph(n, ei, ej, w, deg)
+    prm = params(2, soc=1, sb=2)
+    y0 = api.random_embedding(g.n, 2, 3, g.degree)
+    s = api.PfeSolver(g, prm)  # default switches
+    st = s.make_state(y0)
+    s.run_soc(st, 1, 2)
+    y_default = st.y.copy()
+    setup = s.report()["setup_seconds"]
+    st.close()
+    s.close()
+    host = run(g, prm, y0, False)
+    assert np.array_equal(y_default, host[0])
+    assert setup < 20.0
