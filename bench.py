@@ -512,7 +512,8 @@ def run_bands(args, rank, world, local):
     import torch.distributed as dist
 
     obj = [api.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
     torch.cuda.set_device(local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     solver = api.BandSolver(g, prm, obj[0], world, rank, device=local, warn=False)
@@ -591,6 +592,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=150.0, help="seconds of timed inner-loop work "
                     "for --impl reference (at least one inner iteration per step)")
     ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--bands", action="store_true", help="N=1: run the sharded (row-band / vertex-range) arm "
+                    "with a one-rank NCCL communicator (the code path torchrun takes for N>1)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas even for the "
                     "sharded configurations")
     args = ap.parse_args()
@@ -598,7 +601,7 @@ def main():
     rank, world, local = dist_init()
     if args.impl == "reference":
         line = run_reference(args, rank, world)
-    elif world > 1 and args.config in SHARDED and not args.replicas:
+    elif (world > 1 or args.bands) and args.config in SHARDED and not args.replicas:
         line = run_bands(args, rank, world, local)
     else:
         line = run_gpu(args, rank, world, local)

@@ -364,8 +364,8 @@ bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, co
     placed = f1;
     for (;;) {
       // every level costs a host round trip: chain-like graphs (thousands of
-      // levels) are left to the host builder as well
-      if (++levels > 4 * max_components) return false;
+      // levels, or levels of a few vertices) are left to the host builder as well
+      if (++levels > 4 * max_components || (levels > 256 && placed < 64L * levels)) return false;
       CKB(cudaMemsetAsync(ncand, 0, sizeof(int), st));
       k_expand<<<blocks_for(f1 - f0), kT, 0, st>>>(f0, f1, jbits, order, iptr, inbr, pos, key, cand, ncand);
       int nc = 0;

@@ -2886,12 +2886,14 @@ int pfe_solver_create_band(const pfe_graph* g, const pfe_params* p, const pfe_ex
                            int32_t nranks, int32_t rank, pfe_solver** out) {
   return guarded([&] {
     require_device(x ? x->device : 0);
+    // (a one-rank team gets a communicator too: its gathers run through NCCL
+    // like any other team's, which is how the one-GPU test box exercises the
+    // process-per-GPU path)
+    if (!nccl_id) config_error("pfe_solver_create_band: null NCCL id");
     ncclComm_t comm = nullptr;
-    if (nranks > 1) {
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof(id));
-      nccl_check(nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
-    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    nccl_check(nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
     try {
       *out = g && g->grid_h > 0 ? create_band_solver(g, p, x, nranks, rank, comm)
                                 : create_range_solver(g, p, x, nranks, rank, comm);

@@ -199,3 +199,29 @@ def test_multi_gpu_one_call_ic0(kind):
     y, rep = api.soc_multi_gpu(g, prm, y0, list(range(gpu_count())), return_report=True)
     assert rep["jacobi_fallback"] == 0
     assert rel(y, api.soc(g, prm, y0)) <= 1e-10
+
+
+# ------------------------------------- one process per GPU (BandSolver) ------
+@pytest.mark.parametrize("kind", ["grid8", "grid24", "knn"])
+def test_band_solver_process_per_gpu_path_one_rank(kind):
+    """The API `bench.py --gpus N` drives under torchrun: pfe_solver_create_band
+    with an NCCL id from rank 0 (ncclCommInitRank), make_state from the global
+    y0, run_soc, the global Y gathered through NCCL.  One rank here (the test
+    box has one GPU): the communicator, the all-gathers of totals / R factors
+    and the Y gather still run through NCCL."""
+    if kind == "knn":
+        g = knn_points_graph(800, 8, 12)
+    else:
+        g = image_graph(33, 47, 9, 1 if kind == "grid8" else 2)
+    d = 4
+    prm = params(d, soc=2, sb=4)
+    y0 = api.random_embedding(g.n, d, 2, g.degree)
+    s = api.BandSolver(g, prm, api.nccl_unique_id(), 1, 0, device=0, warn=False)
+    st = s.make_state(y0)
+    s.run_soc(st, prm.soc_max, prm.sb_max_stage1)
+    y = st.y
+    assert s.last_ms() > 0.0
+    assert s.report()["inner_iterations"] == prm.soc_max * prm.sb_max_stage1
+    st.close()
+    s.close()
+    assert rel(y, api.soc(g, prm, y0, persistent=False)) <= 1e-11
