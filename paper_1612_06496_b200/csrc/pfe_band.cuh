@@ -190,6 +190,110 @@ void setup_team_ic(pfe_solver* S, const HostGraph& hg, const Incidence& inc, con
   }
 }
 
+// The same band arrays derived on the device (round 2): only the edges whose
+// first endpoint lies in the band's rows, plus the R rows above (their
+// weights enter diag(A) of the band's first rows), are uploaded -- a
+// contiguous slice of the lexicographic edge list -- and the slot weights,
+// diag, inv diag, sqrt(deg) and coefficients come from the kernels of the
+// single-GPU grid builder run on that sub-grid.  Per band this costs O(m / P)
+// instead of the O(n + m) host loops of setup_band_grid (C4: ~1.5 s per
+// band), which is what the one-call multi-GPU path pays once per band.
+// Returns false when the slice breaks the grid contract (the caller then
+// takes the host path, which reports the offending edge).
+bool setup_band_grid_device(pfe_solver* S, const HostGraph& g, int gh, int gw, int grad, const BandPlan& bp) {
+  const int S_ = grad == 1 ? 4 : 12;
+  if (!(gh > 0 && gw > 0 && static_cast<long>(gh) * gw == g.n && (grad == 1 || grad == 2) && gw >= 2 * grad + 2))
+    return false;
+  // first endpoints must ascend for the slice search (full order is checked on the slice by the kernel)
+  std::atomic<bool> sorted{true};
+  parallel_for(g.m, [&](long kb, long ke) {
+    for (long k = std::max(1L, kb); k < ke; ++k)
+      if (g.ei[k - 1] > g.ei[k]) {
+        sorted = false;
+        return;
+      }
+  });
+  if (!sorted) return false;
+  const double hl = 0.5 * S->prm.lambda, dterm = 0.5 * S->prm.r;
+  const int elo = std::max(0, bp.lo - grad), ehi = bp.hi;  // rows whose edges are needed
+  const int voff = elo * gw;
+  const long k0 = std::lower_bound(g.ei, g.ei + g.m, voff) - g.ei;
+  const long k1 = std::lower_bound(g.ei, g.ei + g.m, ehi * gw) - g.ei;
+  const long ms = k1 - k0, ne = static_cast<long>(ehi - elo) * gw, nl = static_cast<long>(bp.hi - bp.lo) * gw;
+  const long off = static_cast<long>(bp.lo - elo) * gw;  // local row 0 inside the extended sub-grid
+  cudaStream_t st = S->stream;
+  DevPool tmp;
+  tmp.stream = tmp.fstream = st;
+  int32_t* d_ei = tmp.alloc<int32_t>(static_cast<size_t>(std::max(ms, 1L)));
+  int32_t* d_ej = tmp.alloc<int32_t>(static_cast<size_t>(std::max(ms, 1L)));
+  double* d_w = tmp.alloc<double>(static_cast<size_t>(std::max(ms, 1L)));
+  int* d_bad = tmp.alloc<int>(1);
+  double* wf_e = S->mem.alloc<double>(static_cast<size_t>(ne) * S_);
+  double* deg_e = S->mem.alloc<double>(static_cast<size_t>(ne));
+  double* diag_e = S->mem.alloc<double>(static_cast<size_t>(ne));
+  double* invd_e = S->mem.alloc<double>(static_cast<size_t>(ne));
+  double* sqd_e = S->mem.alloc<double>(static_cast<size_t>(ne));
+  if (ms > 0) {
+    copy_h2d(d_ei, g.ei + k0, sizeof(int32_t) * ms, st);
+    copy_h2d(d_ej, g.ej + k0, sizeof(int32_t) * ms, st);
+    copy_h2d(d_w, g.w + k0, sizeof(double) * ms, st);
+  }
+  copy_h2d(deg_e, g.deg + voff, sizeof(double) * ne, st);
+  CK(cudaMemsetAsync(wf_e, 0, sizeof(double) * ne * S_, st));
+  CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  const int eb = static_cast<int>(std::min<long>(std::max<long>(1, (ms + 255) / 256), 32L * S->sm));
+  if (ms > 0) k_grid_slots<<<eb, 256, 0, st>>>(ms, gw, grad, d_ei, d_ej, d_w, wf_e, nullptr, d_bad, voff);
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // edges of the slice must stay inside the rows the band stores (+ R below)
+  if (bad) {
+    S->mem.release(wf_e);
+    S->mem.release(deg_e);
+    S->mem.release(diag_e);
+    S->mem.release(invd_e);
+    S->mem.release(sqd_e);
+    return false;
+  }
+  const int vb = static_cast<int>(std::max<long>(1, std::min<long>((ne + 255) / 256, 32L * S->sm)));
+  k_grid_diag<<<vb, 256, 0, st>>>(ehi - elo, gw, grad, hl, dterm, S->prm.preconditioner == PFE_PRECOND_NONE, wf_e,
+                                  deg_e, diag_e, invd_e);
+  k_sqrt<<<vb, 256, 0, st>>>(ne, deg_e, sqd_e);
+  CK(cudaGetLastError());
+  S->n = static_cast<int>(nl);
+  S->deg = deg_e + off;
+  S->sqd = sqd_e + off;
+  S->diag = diag_e + off;
+  S->invd = invd_e + off;
+  double* dwf = wf_e + off * S_;
+  S->row_lo = bp.r0 - bp.lo;
+  S->row_hi = bp.r1 - bp.lo;
+  S->part = 1;
+  S->own_vb = static_cast<long>(S->row_lo) * gw;
+  S->own_cnt = (S->row_hi - S->row_lo) * gw;
+  S->band_h = gh;
+  S->band_w = gw;
+  S->band_rad = grad;
+  S->band_r0 = bp.r0;
+  S->band_r1 = bp.r1;
+  S->band_lo = bp.lo;
+  S->edge_rows = nl * S_;
+  const int hloc = bp.hi - bp.lo;
+  double* dcf = grid_coef(S, dwf, nl * S_, hl, st);
+  CK(cudaStreamSynchronize(st));  // the temporaries are freed next
+  if (grad == 1) {
+    S->topo.kind = pfe_host::kTopoGrid1;
+    S->topo.g1 = pfe_dev::Grid<1>{S->n, hloc, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+    S->topo.g1.cf = dcf;
+  } else {
+    S->topo.kind = pfe_host::kTopoGrid2;
+    S->topo.g2 = pfe_dev::Grid<2>{S->n, hloc, gw, hl, dwf, S->diag, S->invd, S->row_lo, S->row_hi};
+    S->topo.g2.cf = dcf;
+  }
+  return true;
+}
+
 pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int nranks, int rank,
                                void* comm) {
   if (!g || !p) config_error("null graph or params");
@@ -211,7 +315,9 @@ pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pf
   S->m = g->m;
   S->global_n = g->n;
   const BandPlan bp = band_plan(g->grid_h, nranks, R, rank);
-  setup_band_grid(S.get(), hg, g->grid_h, g->grid_w, R, bp);
+  const bool host_only = std::getenv("PFE_HOST_TOPOLOGY") && std::getenv("PFE_HOST_TOPOLOGY")[0] == '1';
+  if (host_only || !setup_band_grid_device(S.get(), hg, g->grid_h, g->grid_w, R, bp))
+    setup_band_grid(S.get(), hg, g->grid_h, g->grid_w, R, bp);
   int maxrows = 0;
   for (int q = 0; q < nranks; ++q) {
     const BandPlan b = band_plan(g->grid_h, nranks, R, q);
@@ -243,11 +349,9 @@ pfe_solver* create_band_solver(const pfe_graph* g, const pfe_params* p, const pf
 
 // Band state: y0 is the GLOBAL column-major n x d embedding.
 pfe_state* create_band_state(pfe_solver* S, const double* y0_global) {
+  // the band's rows of every column are contiguous in the global matrix
   const long gn = S->global_n, vb = static_cast<long>(S->band_lo) * S->band_w;
-  std::vector<double> loc(static_cast<size_t>(S->n) * S->d);
-  for (int j = 0; j < S->d; ++j)
-    std::memcpy(loc.data() + static_cast<size_t>(j) * S->n, y0_global + j * gn + vb, sizeof(double) * S->n);
-  return create_state(S, loc.data());
+  return create_state(S, y0_global + vb, gn);
 }
 
 // ------------------------------------------------------------------ team --
@@ -659,6 +763,21 @@ void team_gather_y(Team& t, double* out) {
   const int d = S0->d, P = S0->nranks;
   const long gn = S0->global_n;
   const size_t slot = static_cast<size_t>(S0->max_own) * d;
+  if (!t.emulated && S0->part == 1 && static_cast<int>(t.size()) == P) {
+    // every band lives in this process: each device writes its owned rows
+    // straight into the caller's column-major matrix (its rows of a column
+    // are contiguous there), no gather through a host copy of all of Y
+    for (pfe_state* st : t.st) {
+      pfe_solver* S = on(st->s);
+      const long cnt = S->own_cnt, v0 = static_cast<long>(S->band_r0) * S->band_w;
+      k_rows_to_colmajor<<<S->grid_for(cnt * d), pfe_dev::kBlock, 0, S->stream>>>(cnt, d, st->y + S->own_vb * d,
+                                                                                S->ystage, nullptr);
+      CK(cudaGetLastError());
+      for (int j = 0; j < d; ++j)
+        copy_d2h(out + v0 + j * gn, S->ystage + static_cast<size_t>(j) * cnt, sizeof(double) * cnt, S->stream);
+    }
+    return;
+  }
   std::vector<double> all;
   if (t.emulated) {
     all.assign(slot * P, 0.0);
@@ -693,10 +812,12 @@ void team_gather_y(Team& t, double* out) {
       v0 = static_cast<long>(bp.r0) * S0->band_w;
       cnt = static_cast<long>(bp.r1 - bp.r0) * S0->band_w;
     }
-    for (long i = 0; i < cnt; ++i) {
-      const long v = S0->part == 2 ? S0->range_vertex[S0->range_start[p] + i] : v0 + i;
-      for (int j = 0; j < d; ++j) out[v + j * gn] = all[p * slot + static_cast<size_t>(i) * d + j];
-    }
+    parallel_for(cnt, [&](long ib, long ie) {
+      for (long i = ib; i < ie; ++i) {
+        const long v = S0->part == 2 ? S0->range_vertex[S0->range_start[p] + i] : v0 + i;
+        for (int j = 0; j < d; ++j) out[v + j * gn] = all[p * slot + static_cast<size_t>(i) * d + j];
+      }
+    }, 1L << 14);
   }
 }
 

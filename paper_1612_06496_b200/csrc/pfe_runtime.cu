@@ -785,12 +785,14 @@ namespace {
 // (dy, dx) from j - i, no wrap-around -- written as slot weights wf[i*S + s]
 // and the edge -> slot map; any edge that breaks the grid contract sets
 // *bad (the host then builds the general CSR topology instead).
+// (voff: first vertex of the sub-grid the slot arrays describe, 0 for the
+// whole image; row bands pass the edges of their rows only.  slot may be null.)
 __global__ void k_grid_slots(long m, int gw, int grad, const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
                              const double* __restrict__ w, double* __restrict__ wf, int32_t* __restrict__ slot,
-                             int* __restrict__ bad) {
+                             int* __restrict__ bad, int voff = 0) {
   const int S_ = grad == 1 ? 4 : 12;
   for (long k = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int i = __ldg(ei + k), j = __ldg(ej + k);
+    const int i = __ldg(ei + k) - voff, j = __ldg(ej + k) - voff;
     bool ok = true;
     if (k > 0) {
       const int pi = __ldg(ei + k - 1), pj = __ldg(ej + k - 1);
@@ -816,7 +818,7 @@ __global__ void k_grid_slots(long m, int gw, int grad, const int32_t* __restrict
       continue;
     }
     const int32_t row = i * S_ + s;
-    slot[k] = row;
+    if (slot) slot[k] = row;
     wf[row] = __ldg(w + k);
   }
 }
@@ -1842,8 +1844,14 @@ __global__ void k_scale_rows(long n, int d, const double* __restrict__ s, const 
 }
 
 // host col-major n x d -> device row-major via a staging buffer
-void upload_rows(pfe_solver* S, const double* host, long n, int d, double* dst, double* staging) {
-  copy_h2d(staging, host, sizeof(double) * n * d, S->stream);
+// (ld: distance between the host columns, n when they are contiguous; a row
+// band uploads its rows of each column of the global matrix)
+void upload_rows(pfe_solver* S, const double* host, long n, int d, double* dst, double* staging, long ld = 0) {
+  if (ld == 0 || ld == n) {
+    copy_h2d(staging, host, sizeof(double) * n * d, S->stream);
+  } else {
+    for (int j = 0; j < d; ++j) copy_h2d(staging + j * n, host + j * ld, sizeof(double) * n, S->stream);
+  }
   k_colmajor_to_rows<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, staging, dst,
                                                                              n == S->n ? S->perm_d : nullptr);
   CK(cudaGetLastError());
@@ -1870,7 +1878,7 @@ void state_init_from_y0(pfe_state* st) {
   st->rq_valid = false;
 }
 
-pfe_state* create_state(pfe_solver* S, const double* y0_host) {
+pfe_state* create_state(pfe_solver* S, const double* y0_host, long y0_ld = 0) {
   auto st = std::make_unique<pfe_state>();
   st->s = S;
   st->device = S->device;
@@ -1894,7 +1902,7 @@ pfe_state* create_state(pfe_solver* S, const double* y0_host) {
   CK(cudaMemsetAsync(st->eb[0], 0, sizeof(double) * ed, S->stream));
   CK(cudaMemsetAsync(st->eb[1], 0, sizeof(double) * ed, S->stream));
   CK(cudaMemsetAsync(st->es, 0, sizeof(double) * ed, S->stream));
-  upload_rows(S, y0_host, S->n, S->d, st->y0, st->q);
+  upload_rows(S, y0_host, S->n, S->d, st->y0, st->q, y0_ld);
   state_init_from_y0(st.get());
   CK(cudaStreamSynchronize(S->stream));
   return st.release();
@@ -2948,8 +2956,29 @@ int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec*
         config_error("pfe_solve_multi_gpu: devices must be distinct (pfe_solve_banded emulates bands on one device)");
     }
     for (int dv : devs) require_device(dv);
-    std::vector<ncclComm_t> comms(ndev, nullptr);
-    nccl_check(nccl().CommInitAll(comms.data(), ndev, devs.data()), "ncclCommInitAll");
+    // PFE_E2E_TIMING=1: wall time of each stage on stderr
+    const bool timing = std::getenv("PFE_E2E_TIMING") && std::getenv("PFE_E2E_TIMING")[0] == '1';
+    auto tprev = std::chrono::steady_clock::now();
+    auto stage = [&](const char* what) {
+      if (!timing) return;
+      const auto tn = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "pfe_solve_multi_gpu: %-14s %.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(tn - tprev).count());
+      tprev = tn;
+    };
+    // communicators are kept per device list for the life of the process:
+    // ncclCommInitAll + destroy cost 0.1-0.5 s per call
+    static std::mutex comm_mu;
+    static std::map<std::vector<int>, std::vector<ncclComm_t>> comm_cache;
+    std::unique_lock<std::mutex> comm_lock(comm_mu);  // one multi-GPU call at a time per process
+    auto cit = comm_cache.find(devs);
+    if (cit == comm_cache.end()) {
+      std::vector<ncclComm_t> fresh(ndev, nullptr);
+      nccl_check(nccl().CommInitAll(fresh.data(), ndev, devs.data()), "ncclCommInitAll");
+      cit = comm_cache.emplace(devs, fresh).first;
+    }
+    const std::vector<ncclComm_t>& comms = cit->second;
+    stage("ncclCommInitAll");
     const bool grid = g->grid_h > 0;
     std::vector<pfe_solver*> solvers(ndev, nullptr);
     std::vector<pfe_state*> states(ndev, nullptr);
@@ -2961,9 +2990,8 @@ int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec*
         }
         if (solvers[b]) {
           cudaSetDevice(solvers[b]->device);
-          delete solvers[b];  // destroys its communicator
-        } else if (comms[b]) {
-          nccl().CommDestroy(comms[b]);
+          solvers[b]->comm = nullptr;  // cached, not owned
+          delete solvers[b];
         }
       }
     };
@@ -2974,7 +3002,9 @@ int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec*
         xb.device = devs[b];
         solvers[b] = grid ? create_band_solver(g, p, &xb, ndev, b, comms[b])
                           : create_range_solver(g, p, &xb, ndev, b, comms[b]);
+        stage("create solver");
         states[b] = grid ? create_band_state(solvers[b], y0) : create_range_state(solvers[b], y0);
+        stage("create state");
         t.st.push_back(states[b]);
       }
       for (auto* S : solvers) CK(cudaEventRecord(on(S)->ev0, S->stream));
@@ -2994,13 +3024,16 @@ int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec*
       }
       for (auto* S : solvers) S->last_ms = worst;  // device time, max over the GPUs
       if (device_ms) *device_ms = worst;
+      stage("solve");
       team_gather_y(t, y_out);
+      stage("gather Y");
       if (rep && pfe_solver_report(solvers[0], rep) != PFE_OK) throw Error(PFE_CUDA_ERROR, g_last_error);
     } catch (...) {
       cleanup();
       throw;
     }
     cleanup();
+    stage("destroy");
   });
 }
 
