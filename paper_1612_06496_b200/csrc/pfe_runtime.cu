@@ -2997,15 +2997,31 @@ int pfe_solve_multi_gpu(const pfe_graph* g, const pfe_params* p, const pfe_exec*
     };
     try {
       Team t;
-      for (int b = 0; b < ndev; ++b) {
-        pfe_exec xb = x ? *x : pfe_exec_default();
-        xb.device = devs[b];
-        solvers[b] = grid ? create_band_solver(g, p, &xb, ndev, b, comms[b])
-                          : create_range_solver(g, p, &xb, ndev, b, comms[b]);
-        stage("create solver");
-        states[b] = grid ? create_band_state(solvers[b], y0) : create_range_state(solvers[b], y0);
-        stage("create state");
-        t.st.push_back(states[b]);
+      {
+        // every band's solver and state are built on their own host thread
+        // (their set-up is per-device work plus host loops over the band's
+        // part of the graph), so the set-up time of a call does not grow with
+        // the number of GPUs
+        nccl();  // loaded before the threads start
+        std::vector<std::exception_ptr> errs(ndev);
+        std::vector<std::thread> workers;
+        for (int b = 0; b < ndev; ++b)
+          workers.emplace_back([&, b] {
+            try {
+              pfe_exec xb = x ? *x : pfe_exec_default();
+              xb.device = devs[b];
+              solvers[b] = grid ? create_band_solver(g, p, &xb, ndev, b, comms[b])
+                                : create_range_solver(g, p, &xb, ndev, b, comms[b]);
+              states[b] = grid ? create_band_state(solvers[b], y0) : create_range_state(solvers[b], y0);
+            } catch (...) {
+              errs[b] = std::current_exception();
+            }
+          });
+        for (auto& w : workers) w.join();
+        for (int b = 0; b < ndev; ++b)
+          if (errs[b]) std::rethrow_exception(errs[b]);
+        for (int b = 0; b < ndev; ++b) t.st.push_back(states[b]);
+        stage("create solvers + states");
       }
       for (auto* S : solvers) CK(cudaEventRecord(on(S)->ev0, S->stream));
       team_run_soc(t, p->soc_max, p->sb_max_stage1);
