@@ -16,6 +16,8 @@
 // 1e-12 threshold; the result is the same unique polar factor.
 #pragma once
 
+#include <utility>
+
 #include "pfe_device.cuh"
 
 namespace pfe_dev {
@@ -48,40 +50,55 @@ __device__ __forceinline__ void block_allsum(double (&x)[NV]) {
 
 // In-place Householder QR of the kQrRows x D matrix whose row t lives in
 // thread t's registers.  Afterwards rows 0..D-1 hold R, the rest are zero.
+//
+// Step K reduces over the block only what it needs: sum_{t>K} a_tK^2 and
+// sum_{t>K} a_tK a_tj for j > K (D - K values), and takes row K from shared
+// memory, written by thread K.  (Round 1 all-reduced 1 + 2D values in every
+// step -- the unused dot products and row K as a sum of one value and 255
+// zeros -- and the kernel was bound by its shuffles: C4 5.0 ms per
+// projection.  The reduced values keep their summation tree and the
+// broadcast its rounding -- "+ 0.0" is what summing a value with zeros does
+// to -0.0 -- so R is bit for bit what it was.)
+template <int D, int K>
+__device__ __forceinline__ void householder_step(double (&row)[D], double (&bc)[D][D]) {
+  constexpr int NV = D - K;
+  const int t = threadIdx.x;
+  double red[NV];  // [0]: sum_{t>K} a_tK^2 ; [j-K]: sum_{t>K} a_tK a_tj, j = K+1..D-1
+#pragma unroll
+  for (int i = 0; i < NV; ++i) red[i] = 0.0;
+  if (t > K) {
+    red[0] = row[K] * row[K];
+#pragma unroll
+    for (int j = K + 1; j < D; ++j) red[j - K] = row[K] * row[j];
+  } else if (t == K) {
+#pragma unroll
+    for (int j = K; j < D; ++j) bc[K][j] = row[j] + 0.0;
+  }
+  block_allsum<NV>(red);  // (its barriers also publish bc[K])
+  const double x0 = bc[K][K];
+  const double nrm = sqrt(x0 * x0 + red[0]);
+  if (nrm == 0.0) return;  // zero column: nothing to annihilate
+  const double alpha = x0 > 0.0 ? -nrm : nrm;
+  const double v0 = x0 - alpha;
+  const double tau = 2.0 / (v0 * v0 + red[0]);
+  const double vt = (t == K) ? v0 : (t > K ? row[K] : 0.0);
+  if (t >= K) {
+#pragma unroll
+    for (int j = K + 1; j < D; ++j) {
+      const double wj = v0 * bc[K][j] + red[j - K];
+      row[j] -= tau * wj * vt;
+    }
+    row[K] = (t == K) ? alpha : 0.0;
+  }
+}
+template <int D, int... Ks>
+__device__ __forceinline__ void householder_steps(double (&row)[D], double (&bc)[D][D], std::integer_sequence<int, Ks...>) {
+  (householder_step<D, Ks>(row, bc), ...);
+}
 template <int D>
 __device__ __forceinline__ void householder_fold(double (&row)[D]) {
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    // [0]: sum_{t>k} a_tk^2 ; [1+j]: sum_{t>k} a_tk a_tj ; [1+D+j]: a_kj (row k broadcast)
-    double red[1 + 2 * D];
-#pragma unroll
-    for (int i = 0; i < 1 + 2 * D; ++i) red[i] = 0.0;
-    if (t > k) {
-      red[0] = row[k] * row[k];
-#pragma unroll
-      for (int j = k + 1; j < D; ++j) red[1 + j] = row[k] * row[j];
-    } else if (t == k) {
-#pragma unroll
-      for (int j = k; j < D; ++j) red[1 + D + j] = row[j];
-    }
-    block_allsum<1 + 2 * D>(red);
-    const double x0 = red[1 + D + k];
-    const double nrm = sqrt(x0 * x0 + red[0]);
-    if (nrm == 0.0) continue;  // zero column: nothing to annihilate
-    const double alpha = x0 > 0.0 ? -nrm : nrm;
-    const double v0 = x0 - alpha;
-    const double tau = 2.0 / (v0 * v0 + red[0]);
-    const double vt = (t == k) ? v0 : (t > k ? row[k] : 0.0);
-    if (t >= k) {
-#pragma unroll
-      for (int j = k + 1; j < D; ++j) {
-        const double wj = v0 * red[1 + D + j] + red[1 + j];
-        row[j] -= tau * wj * vt;
-      }
-      row[k] = (t == k) ? alpha : 0.0;
-    }
-  }
+  __shared__ double bc[D][D];  // row K of step K (columns K..D-1)
+  householder_steps<D>(row, bc, std::make_integer_sequence<int, D>{});
 }
 
 // A row: sqd ? (sqrt(d_v) * y_v + B_v) : y_v   (solver.cpp:116-117)
@@ -260,30 +277,42 @@ __global__ void __launch_bounds__(kBlock) k_project_apply(int n, const double* _
   for (int i = threadIdx.x; i < D * D; i += blockDim.x) W[i] = wmat[i];
   __syncthreads();
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  // one row per thread, moved as whole 16 / 32-byte pieces (the scalar
+  // version wrote three arrays 8 bytes at a time from 32 rows per warp)
   for (long v = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
     double dy[D], a[D];
+    const Row<D> yr = ldg_row<D>(y + v * D);
+    Row<D> br;
+    double sq = 0.0;
     if (sqd) {
-      const double s = __ldg(sqd + v);
+      sq = __ldg(sqd + v);
+      br = ld_row<D>(breg + v * D);
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        dy[k] = s * __ldg(y + v * D + k);
-        a[k] = dy[k] + breg[v * D + k];
+        dy[k] = sq * yr.a[k];
+        a[k] = dy[k] + br.a[k];
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < D; ++k) a[k] = __ldg(y + v * D + k);
+      for (int k = 0; k < D; ++k) a[k] = yr.a[k];
     }
+    Row<D> po, bnew, rqv;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < D; ++k) s += a[k] * W[k * D + j];
-      pout[v * D + j] = s;
+      po.a[j] = s;
       if (sqd) {
-        const double bn = breg[v * D + j] + (dy[j] - s);
-        breg[v * D + j] = bn;
-        rq[v * D + j] = hr * (__ldg(sqd + v) * (s - bn));
+        const double bn = br.a[j] + (dy[j] - s);
+        bnew.a[j] = bn;
+        rqv.a[j] = hr * (sq * (s - bn));
       }
+    }
+    st_row<D>(pout + v * D, po);
+    if (sqd) {
+      st_row<D>(breg + v * D, bnew);
+      st_row<D>(rq + v * D, rqv);
     }
   }
 }
