@@ -105,13 +105,15 @@ __device__ __forceinline__ void householder_fold(double (&row)[D]) {
 template <int D>
 __device__ __forceinline__ void load_a_row(double (&row)[D], long v, const double* __restrict__ y,
                                            const double* __restrict__ sqd, const double* __restrict__ breg) {
+  const Row<D> yr = ldg_row<D>(y + v * D);  // the row as 16 / 32-byte pieces
   if (sqd) {
     const double s = __ldg(sqd + v);
+    const Row<D> br = ldg_row<D>(breg + v * D);
 #pragma unroll
-    for (int k = 0; k < D; ++k) row[k] = s * __ldg(y + v * D + k) + __ldg(breg + v * D + k);
+    for (int k = 0; k < D; ++k) row[k] = s * yr.a[k] + br.a[k];
   } else {
 #pragma unroll
-    for (int k = 0; k < D; ++k) row[k] = __ldg(y + v * D + k);
+    for (int k = 0; k < D; ++k) row[k] = yr.a[k];
   }
 }
 
