@@ -62,7 +62,11 @@ __device__ __forceinline__ void block_allsum(double (&x)[NV]) {
 template <int D, int K>
 __device__ __forceinline__ void householder_step(double (&row)[D], double (&bc)[D][D]) {
   constexpr int NV = D - K;
-  const int t = threadIdx.x;
+  constexpr int NW = kBlock / 32;
+  __shared__ double part[NW][D];  // per-warp sums
+  __shared__ double coef[D + 2];  // [0] alpha, [1] v0, [2..] tau * w_j for j = K+1.., written by warp 0
+  __shared__ int skip;            // zero column: nothing to annihilate
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   double red[NV];  // [0]: sum_{t>K} a_tK^2 ; [j-K]: sum_{t>K} a_tK a_tj, j = K+1..D-1
 #pragma unroll
   for (int i = 0; i < NV; ++i) red[i] = 0.0;
@@ -74,21 +78,48 @@ __device__ __forceinline__ void householder_step(double (&row)[D], double (&bc)[
 #pragma unroll
     for (int j = K; j < D; ++j) bc[K][j] = row[j] + 0.0;
   }
-  block_allsum<NV>(red);  // (its barriers also publish bc[K])
-  const double x0 = bc[K][K];
-  const double nrm = sqrt(x0 * x0 + red[0]);
-  if (nrm == 0.0) return;  // zero column: nothing to annihilate
-  const double alpha = x0 > 0.0 ? -nrm : nrm;
-  const double v0 = x0 - alpha;
-  const double tau = 2.0 / (v0 * v0 + red[0]);
-  const double vt = (t == K) ? v0 : (t > K ? row[K] : 0.0);
+  // the same tree as block_allsum: warp butterfly, then the warps in order
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[i] += __shfl_xor_sync(0xffffffffu, red[i], o);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) part[warp][i] = red[i];
+  __syncthreads();
+  // Warp 0 finishes the totals and the step's scalars once for the block
+  // (every thread used to repeat the 8 * NV additions, the square root and
+  // the division; the FP64 pipe was the kernel's limit): lane i owns total i.
+  if (warp == 0) {
+    double tot = 0.0;
+    if (lane < NV)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) tot += part[w][lane];
+    double v0 = 0.0, tau = 0.0;
+    if (lane == 0) {
+      const double x0 = bc[K][K];
+      const double nrm = sqrt(x0 * x0 + tot);
+      skip = nrm == 0.0 ? 1 : 0;
+      const double alpha = x0 > 0.0 ? -nrm : nrm;
+      v0 = x0 - alpha;
+      tau = 2.0 / (v0 * v0 + tot);
+      coef[0] = alpha;
+      coef[1] = v0;
+    }
+    v0 = __shfl_sync(0xffffffffu, v0, 0);
+    tau = __shfl_sync(0xffffffffu, tau, 0);
+    if (lane >= 1 && lane < NV) {
+      const double wj = v0 * bc[K][K + lane] + tot;
+      coef[1 + lane] = tau * wj;
+    }
+  }
+  __syncthreads();
+  if (skip) return;
+  const double vt = (t == K) ? coef[1] : (t > K ? row[K] : 0.0);
   if (t >= K) {
 #pragma unroll
-    for (int j = K + 1; j < D; ++j) {
-      const double wj = v0 * bc[K][j] + red[j - K];
-      row[j] -= tau * wj * vt;
-    }
-    row[K] = (t == K) ? alpha : 0.0;
+    for (int j = K + 1; j < D; ++j) row[j] -= coef[1 + (j - K)] * vt;
+    row[K] = (t == K) ? coef[0] : 0.0;
   }
 }
 template <int D, int... Ks>
