@@ -944,57 +944,115 @@ pfe_solver* create_range_solver(const pfe_graph* g, const pfe_params* p, const p
   for (int l = 0; l < nloc; ++l) S->local_vertex[l] = vat[l < own ? s0 + l : ghost[l - own]];
   // diag(A) from the global incidence (edge order, (r/2) d_v last)
   std::vector<double> diag(nloc), invd(nloc), deg(nloc), sqd(nloc);
-  for (int l = 0; l < nloc; ++l) {
-    const int v = S->local_vertex[l];
-    double acc = 0.0;
-    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) acc += (hl * inc.iw[k]) * inc.iw[k];
-    diag[l] = acc + dterm * g->degree[v];
-    invd[l] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[l] > 0.0 ? 1.0 / diag[l] : 1.0);
-    deg[l] = g->degree[v];
-    sqd[l] = std::sqrt(g->degree[v]);
-  }
-  // A rows of the owned vertices in the reference's column order
-  std::vector<int> aptr(static_cast<size_t>(own) + 1, 0), acol;
-  std::vector<double> aval;
-  std::vector<std::pair<int, double>> row;
+  parallel_for(nloc, [&](long lb, long le) {
+    for (long l = lb; l < le; ++l) {
+      const int v = S->local_vertex[l];
+      double acc = 0.0;
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) acc += (hl * inc.iw[k]) * inc.iw[k];
+      diag[l] = acc + dterm * g->degree[v];
+      invd[l] = S->prm.preconditioner == PFE_PRECOND_NONE ? 1.0 : (diag[l] > 0.0 ? 1.0 / diag[l] : 1.0);
+      deg[l] = g->degree[v];
+      sqd[l] = std::sqrt(g->degree[v]);
+    }
+  }, 4096);
+  // A rows of the owned vertices in the reference's column order: merged in
+  // parallel into an upper-bound layout (degree + 1 entries per row), then
+  // compacted (the single-GPU builder's scheme)
+  std::vector<long> ub(static_cast<size_t>(own) + 1, 0);
   for (int l = 0; l < own; ++l) {
     const int v = S->local_vertex[l];
-    row.clear();
-    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) row.emplace_back(inc.inbr[k], -((hl * inc.iw[k]) * inc.iw[k]));
-    row.emplace_back(v, diag[l]);
-    std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    for (size_t t = 0; t < row.size();) {
-      const int col = row[t].first;
-      double sum = 0.0;
-      if (col == v) {
-        sum = row[t].second;
-        ++t;
-      } else {
-        for (; t < row.size() && row[t].first == col; ++t) sum += row[t].second;
-      }
-      if (sum != 0.0) {
-        acol.push_back(lid(pos[col]));
-        aval.push_back(sum);
-      }
-    }
-    aptr[l + 1] = static_cast<int>(acol.size());
+    ub[l + 1] = ub[l] + (inc.iptr[v + 1] - inc.iptr[v]) + 1;
   }
-  // local edge rows (first visit order) and incidence lists of the owned vertices
-  std::vector<int> erow(static_cast<size_t>(g->m), -1);
-  std::vector<int> iptr2(static_cast<size_t>(own) + 1, 0), inbr2, ieid2;
-  std::vector<double> iw2;
-  int ne = 0;
+  uvec<int> tcol(static_cast<size_t>(ub[own])), tlen(static_cast<size_t>(own));
+  uvec<double> tval(static_cast<size_t>(ub[own]));
+  parallel_for(own, [&](long lb, long le) {
+    std::vector<std::pair<int, double>> row;
+    for (long l = lb; l < le; ++l) {
+      const int v = S->local_vertex[l];
+      row.clear();
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) row.emplace_back(inc.inbr[k], -((hl * inc.iw[k]) * inc.iw[k]));
+      row.emplace_back(v, diag[l]);
+      std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      long at = ub[l];
+      for (size_t t = 0; t < row.size();) {
+        const int col = row[t].first;
+        double sum = 0.0;
+        if (col == v) {
+          sum = row[t].second;
+          ++t;
+        } else {
+          for (; t < row.size() && row[t].first == col; ++t) sum += row[t].second;
+        }
+        if (sum != 0.0) {
+          tcol[static_cast<size_t>(at)] = lid(pos[col]);
+          tval[static_cast<size_t>(at)] = sum;
+          ++at;
+        }
+      }
+      tlen[l] = static_cast<int>(at - ub[l]);
+    }
+  }, 2048);
+  std::vector<int> aptr(static_cast<size_t>(own) + 1, 0);
+  for (int l = 0; l < own; ++l) aptr[l + 1] = aptr[l] + tlen[l];
+  uvec<int> acol(static_cast<size_t>(aptr[own]));
+  uvec<double> aval(static_cast<size_t>(aptr[own]));
+  parallel_for(own, [&](long lb, long le) {
+    for (long l = lb; l < le; ++l) {
+      std::copy(tcol.begin() + ub[l], tcol.begin() + ub[l] + tlen[l], acol.begin() + aptr[l]);
+      std::copy(tval.begin() + ub[l], tval.begin() + ub[l] + tlen[l], aval.begin() + aptr[l]);
+    }
+  }, 4096);
+  // local edge rows (first visit order: vertex by vertex, each in edge order)
+  // and incidence lists of the owned vertices.  An edge is first visited at
+  // its owned endpoint with the smaller local index, so every vertex can
+  // count the edges it visits first; a prefix sum then numbers them.
+  auto local_of = [&](int u) {  // local index if owned, else -1
+    const int pu = pos[u];
+    return pu >= s0 && pu < s1 ? pu - s0 : -1;
+  };
+  std::vector<int> first(static_cast<size_t>(own) + 1, 0), iptr2(static_cast<size_t>(own) + 1, 0);
+  parallel_for(own, [&](long lb, long le) {
+    for (long l = lb; l < le; ++l) {
+      const int v = S->local_vertex[l];
+      int c = 0;
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) {
+        const int lu = local_of(inc.inbr[k]);
+        c += (lu < 0 || lu > l) ? 1 : 0;
+      }
+      first[l + 1] = c;
+      iptr2[l + 1] = inc.iptr[v + 1] - inc.iptr[v];
+    }
+  }, 4096);
   for (int l = 0; l < own; ++l) {
-    const int v = S->local_vertex[l];
-    for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) {
-      const int e = inc.ieid[k], u = inc.inbr[k];
-      if (erow[e] < 0) erow[e] = ne++;
-      inbr2.push_back(lid(pos[u]));
-      ieid2.push_back((erow[e] << 1) | (u > v ? 1 : 0));
-      iw2.push_back(inc.iw[k]);
-    }
-    iptr2[l + 1] = static_cast<int>(inbr2.size());
+    first[l + 1] += first[l];
+    iptr2[l + 1] += iptr2[l];
   }
+  const int ne = first[own];
+  uvec<int> erow(static_cast<size_t>(g->m));  // written for every edge incident to an owned vertex
+  parallel_for(own, [&](long lb, long le) {
+    for (long l = lb; l < le; ++l) {
+      const int v = S->local_vertex[l];
+      int next = first[l];
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k) {
+        const int lu = local_of(inc.inbr[k]);
+        if (lu < 0 || lu > l) erow[inc.ieid[k]] = next++;
+      }
+    }
+  }, 4096);
+  uvec<int> inbr2(static_cast<size_t>(iptr2[own])), ieid2(static_cast<size_t>(iptr2[own]));
+  uvec<double> iw2(static_cast<size_t>(iptr2[own]));
+  parallel_for(own, [&](long lb, long le) {
+    for (long l = lb; l < le; ++l) {
+      const int v = S->local_vertex[l];
+      int at = iptr2[l];
+      for (int k = inc.iptr[v]; k < inc.iptr[v + 1]; ++k, ++at) {
+        const int e = inc.ieid[k], u = inc.inbr[k];
+        inbr2[at] = lid(pos[u]);
+        ieid2[at] = (erow[e] << 1) | (u > v ? 1 : 0);
+        iw2[at] = inc.iw[k];
+      }
+    }
+  }, 4096);
   cudaStream_t st = S->stream;
   S->n = nloc;
   S->deg = S->mem.upload(deg, st);
