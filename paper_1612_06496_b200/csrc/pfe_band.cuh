@@ -542,6 +542,7 @@ void team_gather_rows(Team& t, F&& field) {
 // move unchanged values.  So the chunking changes no result, and a typical
 // solve costs one host round trip instead of one per PCG iteration.
 void team_pcg(Team& t, const std::vector<const double*>& rhs) {
+  NvtxRange nv("pfe band pcg");
   const size_t B = t.size();
   std::vector<PcgArgs> a(B);
   for (size_t i = 0; i < B; ++i) {
@@ -659,6 +660,7 @@ void team_pcg(Team& t, const std::vector<const double*>& rhs) {
 
 // PfeSolver::split_bregman (solver.cpp:73-108) over every band.
 void team_split_bregman(Team& t, int max_iter) {
+  NvtxRange nv("pfe band split_bregman");
   const size_t B = t.size();
   std::vector<const double*> rhs(B);
   for (size_t i = 0; i < B; ++i) {
@@ -705,6 +707,7 @@ void team_split_bregman(Team& t, int max_iter) {
 // Projection (solver.cpp:116-118): TSQR factors of every band folded in rank
 // order on every band, so all bands apply the same W.
 void team_project(Team& t) {
+  NvtxRange nv("pfe band projection");
   const size_t B = t.size();
   const int d = t.S(0)->d;
   const size_t fac = static_cast<size_t>(t.S(0)->qr_blocks) * d * d;
@@ -759,6 +762,7 @@ void team_run_soc(Team& t, int soc_max, int sb_max) {
 
 // Global column-major Y from the owned rows of every band / range.
 void team_gather_y(Team& t, double* out) {
+  NvtxRange nv("pfe band gather Y");
   const pfe_solver* S0 = t.S(0);
   const int d = S0->d, P = S0->nranks;
   const long gn = S0->global_n;

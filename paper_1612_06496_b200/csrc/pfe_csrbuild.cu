@@ -29,9 +29,11 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <climits>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -72,6 +74,12 @@ struct Scratch {
   ~Scratch() {
     for (void* p : ptrs) cudaFreeAsync(p, st);
   }
+};
+
+// NVTX range for a scope (popped on every exit path)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
 };
 
 #define GRID_STRIDE(i, n) for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < (n); i += static_cast<long>(gridDim.x) * blockDim.x)
@@ -310,6 +318,7 @@ bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, co
   void* cub_tmp = tmp.get<char>(cub_bytes);
 
   // ---- incidence lists, natural vertex order, increasing edge index
+  auto nv = std::make_unique<Nvtx>("pfe csr build: incidence");
   int* keys = tmp.get<int>(m2);
   int* vals = tmp.get<int>(m2);
   int* vert = tmp.get<int>(m2);   // sorted keys: the vertex of every incidence entry
@@ -340,6 +349,8 @@ bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, co
   const int jbits = bits_for(std::max(1, maxdeg));
 
   // ---- breadth-first storage order (the sequential queue's order)
+  nv.reset();
+  nv = std::make_unique<Nvtx>("pfe csr build: breadth-first order");
   int* pos = static_cast<int*>(keep(sizeof(int) * n));  // vertex -> storage row (kept: perm)
   int* order = tmp.get<int>(n);
   ull* key = tmp.get<ull>(n);
@@ -386,6 +397,8 @@ bool csr_topology_device(int n, long m, const int32_t* ei, const int32_t* ej, co
   CKB(cudaGetLastError());
 
   // ---- rows of A in storage order
+  nv.reset();
+  nv = std::make_unique<Nvtx>("pfe csr build: rows of A, incidence");
   ull* rkeys = tmp.get<ull>(ent);
   ull* rkeys2 = tmp.get<ull>(ent);
   int* ridx = tmp.get<int>(ent);

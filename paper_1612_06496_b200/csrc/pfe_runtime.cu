@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <unistd.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -106,6 +107,16 @@ void retain_pool_memory(int dev) {
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   done[dev] = true;
 }
+
+// NVTX range for a scope (the reference has no tracer; profilers
+// see the stages of a call as named ranges: `ncu --nvtx --nvtx-include "pfe projection/"`).
+// NVTX 3 is header-only and does nothing unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Process-wide pool of host worker threads for parallel_for: creating 16
 // std::threads per call cost ~0.5 ms, which made the many small parallel
@@ -1781,7 +1792,11 @@ pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exe
   if (!g || !p) config_error("null graph or params");
   const auto t0 = std::chrono::steady_clock::now();
   HostGraph hg{g->n, static_cast<long>(g->m), g->ei, g->ej, g->w, g->degree};
-  validate(hg, *p, true);
+  NvtxRange nv_create("pfe solver create");
+  {
+    NvtxRange nv("pfe validate");
+    validate(hg, *p, true);
+  }
   if (g->m > 0x3fffffffL) config_error("graph too large for 32-bit edge indices");
   auto S = std::make_unique<pfe_solver>();
   S->prm = *p;
@@ -1798,7 +1813,10 @@ pfe_solver* create_solver(const pfe_graph* g, const pfe_params* p, const pfe_exe
   S->n = g->n;
   S->m = g->m;
   const auto t1 = std::chrono::steady_clock::now();
-  build_topology(S.get(), hg, S->ic ? 0 : g->grid_h, S->ic ? 0 : g->grid_w, S->ic ? 0 : g->grid_radius);
+  {
+    NvtxRange nv("pfe topology");
+    build_topology(S.get(), hg, S->ic ? 0 : g->grid_h, S->ic ? 0 : g->grid_w, S->ic ? 0 : g->grid_radius);
+  }
   const auto t2 = std::chrono::steady_clock::now();
   upload_degree(S.get(), g->degree);
   S->qr_blocks = qr_blocks_for(S.get(), g->n);
@@ -1857,6 +1875,7 @@ void upload_rows(pfe_solver* S, const double* host, long n, int d, double* dst, 
   CK(cudaGetLastError());
 }
 void download_rows(pfe_solver* S, const double* src, long n, int d, double* host, double* staging) {
+  NvtxRange nv("pfe download");
   k_rows_to_colmajor<<<S->grid_for(n * d), pfe_dev::kBlock, 0, S->stream>>>(n, d, src, staging,
                                                                              n == S->n ? S->perm_d : nullptr);
   CK(cudaGetLastError());
@@ -1879,6 +1898,7 @@ void state_init_from_y0(pfe_state* st) {
 }
 
 pfe_state* create_state(pfe_solver* S, const double* y0_host, long y0_ld = 0) {
+  NvtxRange nv("pfe state create");
   auto st = std::make_unique<pfe_state>();
   st->s = S;
   st->device = S->device;
@@ -2108,6 +2128,7 @@ int sb_prefetch() {
 
 // PfeSolver::split_bregman (solver.cpp:73-108).
 void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
+  NvtxRange nv("pfe split_bregman");
   pfe_solver* S = st->s;
   const double hl = 0.5 * S->prm.lambda, hr = 0.5 * S->prm.r, gamma = 1.0 / S->prm.lambda;
   const bool conv = S->prm.conv_tol > 0.0;
@@ -2220,6 +2241,7 @@ void split_bregman_run(pfe_state* st, int max_iter, const RunMode& mode) {
 // Projection + outer Bregman update (solver.cpp:116-118) with the next
 // rhs_quad fused into the same pass.
 void project_step(pfe_state* st) {
+  NvtxRange nv("pfe projection");
   pfe_solver* S = st->s;
   S->prof.begin(6, S->stream);
   S->tab->tsqr_local(S->n, st->y, S->sqd, st->breg, S->rbuf, {S->qr_blocks, S->stream});
@@ -2272,6 +2294,7 @@ void execute_inner(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, v
 
 // Device time of every call, CUDA events on the solver stream.
 void execute(pfe_state* st, int kind, int a0, int a1, pfe_iterate_fn cb, void* user) {
+  NvtxRange nv(kind == kCallSplit ? "pfe call split_bregman" : (kind == kCallSoc ? "pfe call run_soc" : "pfe call two_stage"));
   pfe_solver* S = st->s;
   CK(cudaEventRecord(S->ev0, S->stream));
   execute_inner(st, kind, a0, a1, cb, user);
@@ -2678,6 +2701,7 @@ int pfe_solve(const pfe_graph* g, const pfe_params* p, const pfe_exec* x, int32_
       return e && e[0] == '1';
     }();
     auto now = [] { return std::chrono::steady_clock::now(); };
+    NvtxRange nv("pfe_solve");
     auto t0 = now();
     std::unique_ptr<pfe_solver> S(create_solver(g, p, x));
     auto t1 = now();
